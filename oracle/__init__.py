@@ -1,0 +1,99 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+Plain CPU reference for PBNG tip decomposition (arXiv 2110.12511), written from
+the paper.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+`--impl reference` leg may import it.  It shares no code with the CUDA path
+(paper_2110_12511_b200/) and imports nothing from it.
+
+  count(g)            -> uint64 support per u    (oracle.c: oracle_count)
+  count_subset(g, us) -> uint64 support per listed u
+  bup_tip(g)          -> uint64 tip number per u (oracle.c: oracle_bup_tip)
+  brute.*             pure-Python brute force and Definition-2 tip numbers for
+                      tiny graphs (oracle/brute.py)
+
+Parity status: count and bup_tip are pinned by tests/test_oracle.py (brute-force
+4-tuple enumeration, K_{a,b} closed form, Σ_U = Σ_V identity, Definition-2 tip
+numbers, golden graphs).  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def build_lib(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", _LIB, _SRC])
+    return _LIB
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("wedges", ctypes.c_uint64), ("updates", ctypes.c_uint64), ("peeled", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {"wedges": self.wedges, "updates": self.updates, "peeled": self.peeled}
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build_lib())
+        base = [ctypes.c_uint32, ctypes.c_uint32] + [ctypes.c_void_p] * 4
+        _lib.oracle_count.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
+        _lib.oracle_count_subset.argtypes = base + [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                                    ctypes.POINTER(Stats)]
+        _lib.oracle_bup_tip.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
+        for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip):
+            f.restype = ctypes.c_int
+    return _lib
+
+
+def _csr(g):
+    arrs = [np.ascontiguousarray(g.off_u, np.uint64), np.ascontiguousarray(g.adj_u, np.uint32),
+            np.ascontiguousarray(g.off_v, np.uint64), np.ascontiguousarray(g.adj_v, np.uint32)]
+    return arrs, [a.ctypes.data for a in arrs]
+
+
+def count(g, stats: Stats | None = None) -> np.ndarray:
+    """Butterfly support of every u in U (one-sided wedge aggregation)."""
+    keep, ptrs = _csr(g)
+    out = np.zeros(g.nU, np.uint64)
+    st = stats if stats is not None else Stats()
+    if _load().oracle_count(g.nU, g.nV, *ptrs, out.ctypes.data, ctypes.byref(st)):
+        raise MemoryError("oracle_count failed")
+    del keep
+    return out
+
+
+def count_subset(g, us, stats: Stats | None = None) -> np.ndarray:
+    """Butterfly support of the listed u only (same traversal as count)."""
+    keep, ptrs = _csr(g)
+    us = np.ascontiguousarray(us, np.uint32)
+    out = np.zeros(us.shape[0], np.uint64)
+    st = stats if stats is not None else Stats()
+    if _load().oracle_count_subset(g.nU, g.nV, *ptrs, us.ctypes.data, us.shape[0], out.ctypes.data,
+                                   ctypes.byref(st)):
+        raise MemoryError("oracle_count_subset failed")
+    del keep
+    return out
+
+
+def bup_tip(g, stats: Stats | None = None) -> np.ndarray:
+    """Tip number of every u in U by sequential bottom-up peeling."""
+    keep, ptrs = _csr(g)
+    out = np.zeros(g.nU, np.uint64)
+    st = stats if stats is not None else Stats()
+    if _load().oracle_bup_tip(g.nU, g.nV, *ptrs, out.ctypes.data, ctypes.byref(st)):
+        raise MemoryError("oracle_bup_tip failed")
+    del keep
+    return out

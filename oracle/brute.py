@@ -1,0 +1,80 @@
+"""ORACLE (brute force) — TEST INFRASTRUCTURE ONLY.
+
+Pure-Python definitions for tiny graphs (≤ ~12 vertices per side).  These are the
+plain definitions the paper states, written out with no algorithmic shortcut:
+
+  butterflies(g)        every 4-tuple {u,u'} x {v,v'} with all four edges present
+                        (a butterfly = 2,2-biclique).
+  tip_by_definition(g)  theta_u = max k such that u lies in a subgraph H with
+                        U(H) ⊆ U, V(H) = V in which every u in U(H) is in >= k
+                        butterflies of H (Definition 2, tip number
+                        P:469-471).  Every k in [0, max support] is swept
+                        (tip numbers can fall between initial supports).
+  init_support(g, part) butterflies u shares only with vertices of partitions
+                        j >= part[u] (the support initialisation vector,
+                        P:781-786), counted from the 4-tuples.
+"""
+from __future__ import annotations
+
+from itertools import combinations
+
+
+def _adj_sets(g):
+    nu = [set(int(x) for x in g.adj_u[int(g.off_u[u]):int(g.off_u[u + 1])]) for u in range(g.nU)]
+    return nu
+
+
+def butterflies(g):
+    """Returns (per-U counts, per-V counts, total, list of (u,u',v,v') tuples)."""
+    nu = _adj_sets(g)
+    cu = [0] * g.nU
+    cv = [0] * g.nV
+    tuples = []
+    for u, u2 in combinations(range(g.nU), 2):
+        for v, v2 in combinations(range(g.nV), 2):
+            if v in nu[u] and v2 in nu[u] and v in nu[u2] and v2 in nu[u2]:
+                cu[u] += 1
+                cu[u2] += 1
+                cv[v] += 1
+                cv[v2] += 1
+                tuples.append((u, u2, v, v2))
+    return cu, cv, len(tuples), tuples
+
+
+def _support_within(tuples, members):
+    s = {u: 0 for u in members}
+    for (u, u2, _, _) in tuples:
+        if u in members and u2 in members:
+            s[u] += 1
+            s[u2] += 1
+    return s
+
+
+def tip_by_definition(g):
+    """Tip number of every u by Definition 2 (largest k-subgraph containing u)."""
+    cu, _, _, tuples = butterflies(g)
+    theta = [0] * g.nU
+    kmax = max(cu) if cu else 0
+    for k in range(0, kmax + 1):
+        members = set(range(g.nU))
+        while True:
+            s = _support_within(tuples, members)
+            drop = {u for u in members if s[u] < k}
+            if not drop:
+                break
+            members -= drop
+        for u in members:
+            theta[u] = max(theta[u], k)
+    return theta
+
+
+def init_support(g, part):
+    """Butterflies of u shared only with u' whose partition index is >= part[u]."""
+    _, _, _, tuples = butterflies(g)
+    s = [0] * g.nU
+    for (u, u2, _, _) in tuples:
+        if part[u2] >= part[u]:
+            s[u] += 1
+        if part[u] >= part[u2]:
+            s[u2] += 1
+    return s

@@ -1,0 +1,193 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded CPU reference for PBNG tip decomposition
+ * (Lakhotia, Kannan, Prasanna, arXiv 2110.12511).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library.  It shares no code, header, table or helper with the
+ * CUDA path (paper_2110_12511_b200/); the two meet only in the seeded inputs
+ * of graphgen/.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line n.
+ *
+ * Functions
+ *   oracle_count     per-vertex butterfly support of every u in U, by plain
+ *                    wedge traversal u -> v -> u' and C(w,2) per endpoint pair
+ *                    ("combine wedges with common end points",
+ *                    Alg.1 l.17-19 P:417-419 C(wedge_count,2) per endpoint).
+ *   oracle_bup_tip   sequential bottom-up tip peeling (Alg.2
+ *                    P:508-531 specialised to vertices of U as P:493-498
+ *                    describes; update rule max(theta, s - C(w,2)) from
+ *                    Alg.2 l.11 P:526 / S:259; tie-break lowest id, reading g2).
+ *   oracle_count_subset  oracle_count restricted to a list of u (for sampled
+ *                    checks at sizes where the full oracle is too slow).
+ *
+ * Pins (tests/test_oracle.py, -m "not gpu"): brute-force 4-tuple enumeration,
+ * K_{a,b} closed form, sum_U = sum_V identity, tip numbers by Definition 2
+ * on tiny graphs, hand-checked golden graphs.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  uint64_t wedges;   /* (u, v, u') adjacency entries read, u' = u included (g11) */
+  uint64_t updates;  /* support decrements applied */
+  uint64_t peeled;   /* vertices peeled */
+} oracle_stats;
+
+static uint64_t choose2(uint64_t w) { return w * (w - 1) / 2; }
+
+/* support[u] = sum_{u' != u} C(|N_u ∩ N_u'|, 2)  for every u listed in `us`
+ * (or all u when us == NULL).  Aggregation with a dense per-vertex counter
+ * array and a touched list (the paper's private n-element wedge_count array,
+ * P:388-390). */
+int oracle_count_subset(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
+                        const uint64_t* offV, const uint32_t* adjV, const uint32_t* us,
+                        uint64_t nus, uint64_t* support, oracle_stats* st) {
+  (void)nV;
+  uint32_t* cnt = (uint32_t*)calloc(nU ? nU : 1, sizeof(uint32_t));
+  uint32_t* touched = (uint32_t*)malloc((nU ? nU : 1) * sizeof(uint32_t));
+  if (!cnt || !touched) { free(cnt); free(touched); return -1; }
+  uint64_t wedges = 0;
+  uint64_t n = us ? nus : nU;
+  for (uint64_t i = 0; i < n; i++) {
+    uint32_t u = us ? us[i] : (uint32_t)i;
+    uint64_t nt = 0;
+    for (uint64_t e = offU[u]; e < offU[u + 1]; e++) {
+      uint32_t v = adjU[e];
+      for (uint64_t f = offV[v]; f < offV[v + 1]; f++) {
+        uint32_t u2 = adjV[f];
+        wedges++;
+        if (u2 == u) continue;
+        if (cnt[u2]++ == 0) touched[nt++] = u2;
+      }
+    }
+    uint64_t s = 0;
+    for (uint64_t t = 0; t < nt; t++) {
+      s += choose2(cnt[touched[t]]);
+      cnt[touched[t]] = 0;
+    }
+    support[us ? i : u] = s;
+  }
+  if (st) st->wedges += wedges;
+  free(cnt);
+  free(touched);
+  return 0;
+}
+
+int oracle_count(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
+                 const uint64_t* offV, const uint32_t* adjV, uint64_t* support, oracle_stats* st) {
+  return oracle_count_subset(nU, nV, offU, adjU, offV, adjV, NULL, 0, support, st);
+}
+
+/* ---- indexed binary min-heap keyed by (support, id) --------------------- */
+typedef struct {
+  uint32_t* heap;   /* heap[i] = vertex id */
+  uint32_t* pos;    /* pos[u] = index in heap, or UINT32_MAX when popped */
+  const uint64_t* key;
+  uint32_t size;
+} iheap;
+
+static int less_(const iheap* h, uint32_t a, uint32_t b) {
+  return h->key[a] < h->key[b] || (h->key[a] == h->key[b] && a < b);
+}
+static void swap_(iheap* h, uint32_t i, uint32_t j) {
+  uint32_t a = h->heap[i], b = h->heap[j];
+  h->heap[i] = b; h->heap[j] = a;
+  h->pos[b] = i; h->pos[a] = j;
+}
+static void up_(iheap* h, uint32_t i) {
+  while (i > 0) {
+    uint32_t p = (i - 1) / 2;
+    if (!less_(h, h->heap[i], h->heap[p])) break;
+    swap_(h, i, p);
+    i = p;
+  }
+}
+static void down_(iheap* h, uint32_t i) {
+  for (;;) {
+    uint32_t l = 2 * i + 1, r = l + 1, m = i;
+    if (l < h->size && less_(h, h->heap[l], h->heap[m])) m = l;
+    if (r < h->size && less_(h, h->heap[r], h->heap[m])) m = r;
+    if (m == i) break;
+    swap_(h, i, m);
+    i = m;
+  }
+}
+static uint32_t pop_(iheap* h) {
+  uint32_t top = h->heap[0];
+  h->size--;
+  if (h->size) {
+    h->heap[0] = h->heap[h->size];
+    h->pos[h->heap[0]] = 0;
+    down_(h, 0);
+  }
+  h->pos[top] = UINT32_MAX;
+  return top;
+}
+
+/* Sequential bottom-up peeling of U (tip decomposition).
+ *   support <- per-vertex butterfly counts            (Alg.2 l.1)
+ *   while U non-empty:                                 (Alg.2 l.2)
+ *     u <- argmin support (lowest id among ties)       (Alg.2 l.3, g2)
+ *     theta_u <- support_u; remove u                   (Alg.2 l.4)
+ *     for every remaining u' sharing w = |N_u ∩ N_u'| >= 2 common neighbours:
+ *       support_u' <- max(theta_u, support_u' - C(w,2)) (Alg.2 l.11 P:526)
+ * Removed vertices are skipped during traversal (equivalent to deleting their
+ * edges). */
+int oracle_bup_tip(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
+                   const uint64_t* offV, const uint32_t* adjV, uint64_t* theta, oracle_stats* st) {
+  (void)nV;
+  if (nU == 0) return 0;
+  uint64_t* support = (uint64_t*)malloc(nU * sizeof(uint64_t));
+  unsigned char* alive = (unsigned char*)malloc(nU);
+  uint32_t* cnt = (uint32_t*)calloc(nU, sizeof(uint32_t));
+  uint32_t* touched = (uint32_t*)malloc(nU * sizeof(uint32_t));
+  iheap h;
+  h.heap = (uint32_t*)malloc(nU * sizeof(uint32_t));
+  h.pos = (uint32_t*)malloc(nU * sizeof(uint32_t));
+  if (!support || !alive || !cnt || !touched || !h.heap || !h.pos) return -1;
+  oracle_stats local = {0, 0, 0};
+  if (oracle_count(nU, nV, offU, adjU, offV, adjV, support, &local)) return -1;
+
+  h.key = support;
+  h.size = nU;
+  for (uint32_t u = 0; u < nU; u++) { h.heap[u] = u; h.pos[u] = u; alive[u] = 1; }
+  for (int64_t i = (int64_t)nU / 2 - 1; i >= 0; i--) down_(&h, (uint32_t)i);
+
+  while (h.size) {
+    uint32_t u = pop_(&h);
+    uint64_t th = support[u];
+    theta[u] = th;
+    alive[u] = 0;
+    local.peeled++;
+    uint64_t nt = 0;
+    for (uint64_t e = offU[u]; e < offU[u + 1]; e++) {
+      uint32_t v = adjU[e];
+      for (uint64_t f = offV[v]; f < offV[v + 1]; f++) {
+        uint32_t u2 = adjV[f];
+        local.wedges++;
+        if (!alive[u2]) continue;
+        if (cnt[u2]++ == 0) touched[nt++] = u2;
+      }
+    }
+    for (uint64_t t = 0; t < nt; t++) {
+      uint32_t u2 = touched[t];
+      uint64_t w = cnt[u2];
+      cnt[u2] = 0;
+      if (w < 2) continue;
+      uint64_t d = choose2(w);
+      uint64_t s = support[u2];
+      uint64_t ns = (s >= th + d) ? s - d : th; /* max(theta_u, s - d) without wrap */
+      local.updates++;
+      if (ns != s) {
+        support[u2] = ns;
+        up_(&h, h.pos[u2]);
+      }
+    }
+  }
+  if (st) { st->wedges += local.wedges; st->updates += local.updates; st->peeled += local.peeled; }
+  free(support); free(alive); free(cnt); free(touched); free(h.heap); free(h.pos);
+  return 0;
+}

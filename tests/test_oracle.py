@@ -1,0 +1,138 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+The oracle (oracle/oracle.c) is checked against things other than itself:
+  * brute-force 4-tuple butterfly enumeration (oracle/brute.py),
+  * the K_{a,b} closed form: support = theta = (a-1)*C(b,2)  (north_star),
+  * the identity Σ_U support = Σ_V support = 2·#butterflies with the
+    V side computed by running the oracle on the transposed graph,
+  * tip numbers from Definition 2 by exhaustive k sweep,
+  * golden graphs (tests/golden/, each with its citation),
+  * the structured config-2 closed form (noise-free) and monotonicity (noisy).
+A plausible mistake (dropped clamp, C(w,2) vs w^2, self-pair counted, wrong
+side, heap tie-break bug) fails at least one of these.
+"""
+import os
+from math import comb
+
+import numpy as np
+import pytest
+
+import graphgen as gg
+import oracle
+from oracle import brute
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _parse(path):
+    rows = []
+    for line in open(path):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        rows.append([c.strip() for c in line.split("|")])
+    return rows
+
+
+def _edges(s):
+    return [tuple(int(x) for x in t.split("-")) for t in s.split()]
+
+
+def _tiny_corpus(n=300, seed0=1000):
+    rng = np.random.default_rng(7)
+    for i in range(n):
+        nu = int(rng.integers(1, 10))
+        nv = int(rng.integers(1, 10))
+        m = int(rng.integers(0, nu * nv + 1))
+        yield gg.uniform(nu, nv, m, seed=seed0 + i)
+
+
+def test_spec_small_cases():
+    for name, sizes, edges, side, sup, th in _parse(os.path.join(GOLD, "spec_small_cases.txt")):
+        nu, nv = map(int, sizes.split())
+        g = gg.from_edges(nu, nv, _edges(edges))
+        if side == "V":
+            g = g.swapped()
+        assert list(oracle.count(g)) == [int(x) for x in sup.split()], name
+        assert list(oracle.bup_tip(g)) == [int(x) for x in th.split()], name
+
+
+def test_survey_golden_graphs():
+    for name, sizes, edges, sup, total, th in _parse(os.path.join(GOLD, "survey_graphs.txt")):
+        nu, nv = map(int, sizes.split())
+        g = gg.from_edges(nu, nv, _edges(edges))
+        s = oracle.count(g)
+        assert list(s) == [int(x) for x in sup.split()], name
+        assert int(s.sum()) == 2 * int(total), name
+        assert list(oracle.bup_tip(g)) == [int(x) for x in th.split()], name
+        assert brute.tip_by_definition(g) == [int(x) for x in th.split()], name
+
+
+@pytest.mark.parametrize("a", range(1, 7))
+@pytest.mark.parametrize("b", range(1, 7))
+def test_complete_bipartite_closed_form(a, b):
+    g = gg.complete(a, b)
+    want = (a - 1) * comb(b, 2)
+    assert list(oracle.count(g)) == [want] * a
+    assert list(oracle.bup_tip(g)) == [want] * a
+    # the V side of K_{a,b} is K_{b,a} seen from the other side
+    assert list(oracle.bup_tip(g.swapped())) == [(b - 1) * comb(a, 2)] * b
+
+
+def test_count_equals_bruteforce_4tuples():
+    for g in _tiny_corpus():
+        cu, cv, total, _ = brute.butterflies(g)
+        su = oracle.count(g)
+        sv = oracle.count(g.swapped())
+        assert list(su) == cu
+        assert list(sv) == cv
+        assert int(su.sum()) == int(sv.sum()) == 2 * total
+
+
+def test_bup_equals_definition2():
+    for g in _tiny_corpus(n=200, seed0=5000):
+        th = oracle.bup_tip(g)
+        assert list(th) == brute.tip_by_definition(g)
+        assert np.all(th <= oracle.count(g))  # theta_u <= support_u
+        thv = oracle.bup_tip(g.swapped())
+        assert list(thv) == brute.tip_by_definition(g.swapped())
+
+
+def test_bup_invariant_under_relabeling():
+    # Lemma 1: theta does not depend on the peel order among ties;
+    # relabel U by a random permutation (changes the lowest-id tie-break).
+    rng = np.random.default_rng(3)
+    for g in _tiny_corpus(n=100, seed0=9000):
+        perm = rng.permutation(g.nU)
+        e = g.edges().astype(np.int64)
+        h = gg.from_edges(g.nU, g.nV, np.stack([perm[e[:, 0]], e[:, 1]], 1))
+        assert np.array_equal(oracle.bup_tip(h)[perm], oracle.bup_tip(g))
+
+
+def test_config2_blocks_closed_form():
+    shapes = gg.block_sizes(200, 5, 60, seed=2)
+    want = np.concatenate([[(a - 1) * comb(b, 2)] * a for a, b in shapes]).astype(np.uint64)
+    g0, _ = gg.config("2a")
+    assert g0.m == sum(a * b for a, b in shapes)
+    assert np.array_equal(oracle.count(g0), want)
+    assert np.array_equal(oracle.bup_tip(g0), want)
+    # with noise edges added, tip numbers can only grow (monotonicity, SURVEY §8(c) θ (iii))
+    g, _ = gg.config(2)
+    assert g.nU == g0.nU and g.m > g0.m
+    th = oracle.bup_tip(g)
+    assert np.all(th >= want)
+
+
+def test_count_subset_matches_count():
+    g, _ = gg.config(1)
+    full = oracle.count(g)
+    us = np.array([0, 5, 17, 1999, 3], np.uint32)
+    assert np.array_equal(oracle.count_subset(g, us), full[us])
+
+
+def test_empty_and_degenerate():
+    g = gg.from_edges(3, 4, [])
+    assert list(oracle.count(g)) == [0, 0, 0]
+    assert list(oracle.bup_tip(g)) == [0, 0, 0]
+    g = gg.from_edges(0, 0, [])
+    assert oracle.bup_tip(g).shape == (0,)
