@@ -1,0 +1,135 @@
+/*
+ * pbng.h — C ABI of the B200-native PBNG tip-decomposition hot path.
+ *
+ * Method: Lakhotia, Kannan, Prasanna, "Parallel Peeling of Bipartite Networks
+ * for Hierarchical Dense Subgraph Discovery" (arXiv 2110.12511).
+ * Citations: "P:n" = line n of the paper text (reference PAPER.md).
+ *
+ * All compute runs in hand-written sm_100a CUDA kernels (libpbng.so).  No
+ * torch types cross this boundary: plain pointers and sizes only.
+ *
+ * Conventions shared by every entry point
+ *   Graph      G(W = (U, V), E), bipartite (Table 1), given as TWO
+ *              CSRs of the same edge set:
+ *                U.offsets[U.n + 1] (uint64), U.indices[U.m] (uint32 ids in V)
+ *                V.offsets[V.n + 1] (uint64), V.indices[V.m] (uint32 ids in U)
+ *              offsets[0] = 0, non-decreasing, offsets[n] = m; U.m == V.m;
+ *              no duplicate edges; the two CSRs are transposes of each other.
+ *              Adjacency order within a list is free (not required sorted).
+ *   side       0: peel U (arguments as given); 1: peel V (roles swapped).
+ *              "peel side" below means U for side 0 and V for side 1
+ *              (tip decomposition peels one vertex set).
+ *   Memory     pbng_* (except *_host) take DEVICE pointers for the graph and
+ *              the outputs, caller-allocated and caller-owned.  The library
+ *              allocates its own scratch stream-ordered on `stream` and frees
+ *              it before returning; it keeps no global state between calls.
+ *   stream     a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   Sync       every call returns only after its work on `stream` completed
+ *              (the CD loop reads counters back to the host), so outputs are
+ *              valid on return.
+ *   Errors     PBNG_OK on success.  PBNG_ERR_ARG: null pointer, bad side,
+ *              P < 1 or P > PBNG_MAX_P, U.m != V.m, size mismatch.
+ *              PBNG_ERR_GRAPH: CSR precondition violated (only detected with
+ *              PBNG_OPT_VALIDATE).  PBNG_ERR_OOM: scratch allocation failed.
+ *              PBNG_ERR_CUDA: any other CUDA error.  On error output contents
+ *              are unspecified; pbng_last_error() returns a thread-local
+ *              message.  No exceptions cross the ABI.
+ *   Integers   ids uint32 (n < 2^32 - 1), counts / supports / tip numbers
+ *              uint64 (tip numbers reach 3e12 in the paper's data).
+ */
+#ifndef PBNG_H
+#define PBNG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBNG_MAX_P 4096u
+
+typedef struct {
+  const uint64_t* offsets; /* n + 1 entries */
+  const uint32_t* indices; /* m entries */
+  uint32_t n;              /* vertices on this side */
+  uint64_t m;              /* edges */
+} pbng_csr;
+
+/* Work / time counters of one decomposition (filled when stats != NULL).
+ * "wedges" = (u, v, u') adjacency entries read, u' = u included. */
+typedef struct {
+  uint64_t wedges_count;     /* initial butterfly count */
+  uint64_t wedges_cd;        /* CD peel iterations + re-counts */
+  uint64_t wedges_fd;        /* FD peeling */
+  uint64_t support_updates;  /* C(w,2) decrements applied (w >= 2 pairs) */
+  uint32_t rho_cd_iters;     /* CD peeling iterations = synchronisation rounds */
+  uint32_t recounts;         /* batch re-count branches taken */
+  uint32_t partitions_used;  /* <= P (fewer when supports run out) */
+  uint32_t fd_rounds_max;    /* most level rounds any FD partition needed */
+  float ms_count, ms_cd, ms_fd_build, ms_fd; /* device time per phase */
+} pbng_stats;
+
+enum {
+  PBNG_OK = 0,
+  PBNG_ERR_ARG = 1,
+  PBNG_ERR_GRAPH = 2,
+  PBNG_ERR_OOM = 3,
+  PBNG_ERR_CUDA = 4
+};
+
+enum {
+  PBNG_OPT_NO_RECOUNT = 1,     /* never take the batch re-count branch (PBNG--) */
+  PBNG_OPT_NO_DELETE = 2,      /* no dynamic edge deletion during CD (PBNG-) */
+  PBNG_OPT_VALIDATE = 4,       /* O(m) CSR precondition check -> PBNG_ERR_GRAPH */
+  PBNG_OPT_STATS = 8,          /* count wedges / updates on device (small overhead) */
+  PBNG_OPT_FORCE_RECOUNT = 16  /* test hook: take the re-count branch every CD iteration */
+};
+
+/* Per-vertex butterfly counts of the peel side:
+ *   out_support[u] = sum_{u' != u} C(|N_u ∩ N_u'|, 2)   (= ⋈_u, Table 1)
+ * computed by wedge aggregation (Alg.1 per-vertex part,
+ * P:417-419).  out_support: device, peel-side n entries. */
+int pbng_count_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_support, void* stream);
+
+/* Tip decomposition of the peel side (tip number θ_u):
+ *   count (Alg.1) -> coarse-grained decomposition CD into <= P ranges
+ *   (Alg.4 structure P:792-816, tip specialisation P:982-991, adaptive range
+ *   P:895-944, batch re-count P:1442-1449, dynamic deletion P:1493-1504)
+ *   -> fine-grained decomposition FD of every partition independently on its
+ *   induced subgraph G_i with LPT-ordered dynamic
+ *   scheduling.
+ * out_tip: device, peel-side n entries (θ = 0 for vertices in no butterfly).
+ * P: number of partitions, 1 <= P <= PBNG_MAX_P (the paper uses 150).
+ * opts: PBNG_OPT_* bit set.  stats: host pointer or NULL. */
+int pbng_tip_decompose(pbng_csr U, pbng_csr V, int side, uint32_t P, uint64_t* out_tip,
+                       uint32_t opts, pbng_stats* stats, void* stream);
+
+/* Same as pbng_tip_decompose but the CSR arrays (U/V offsets and indices) and
+ * out_tip are HOST pointers (pinned memory recommended).  Host->device copies,
+ * the decomposition and the device->host copy of θ all run on `stream`
+ * inside this call; device buffers are allocated and freed internally. */
+int pbng_tip_decompose_host(pbng_csr U, pbng_csr V, int side, uint32_t P, uint64_t* out_tip,
+                            uint32_t opts, pbng_stats* stats, void* stream);
+
+/* Test hook: run count + CD only and return the partition plan.
+ *   out_part[u]  partition index i in [0, *out_nparts) (device, n entries)
+ *   out_init[u]  ⋈^init_u: support of u at the start of its partition
+ *                 (device, n entries)
+ *   out_bounds   θ(1..P+1) range bounds, HOST array of P + 1 entries:
+ *                bounds[0] = 0 < bounds[1] < ... < bounds[nparts] = UINT64_MAX;
+ *                entries past nparts are set to UINT64_MAX.
+ *   out_nparts   HOST pointer, partitions produced. */
+int pbng_tip_plan(pbng_csr U, pbng_csr V, int side, uint32_t P, uint32_t opts, uint32_t* out_part,
+                  uint64_t* out_init, uint64_t* out_bounds, uint32_t* out_nparts, void* stream);
+
+/* Message for the last non-OK return on this thread ("" if none). */
+const char* pbng_last_error(void);
+
+/* Library version string, e.g. "pbng-b200 0.1 sm_100a". */
+const char* pbng_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBNG_H */

@@ -1,0 +1,550 @@
+// kernels_cd.cuh — counting and coarse-grained decomposition (CD) kernels.
+//
+// Paper: Lakhotia, Kannan, Prasanna, arXiv 2110.12511 ("P:n" = PAPER.md line).
+//   wedge aggregation / counting     P:369-391, Alg.1
+//   CD tip peeling                   P:743-790, Alg.4, tip P:982-991
+//   range determination              P:818-826, tip P:1387-1391
+//   batch re-count
+//   dynamic graph updates
+#pragma once
+#include "device_common.cuh"
+
+namespace pbng {
+
+// Per-warp / per-CTA hash capacities (slots are power-of-two; load factor <= 1/2).
+constexpr uint32_t kWarpSlots = 1024;           // tier 0: one warp per u
+constexpr uint32_t kWarpCap = kWarpSlots / 2;   // partners bound for tier 0
+constexpr uint32_t kCtaSlots = 16384;           // tier 1: one CTA per u
+constexpr uint32_t kCtaCap = kCtaSlots / 2;     // partners bound for tier 1
+constexpr uint32_t kWarpTierThreads = 256;
+constexpr uint32_t kCtaTierThreads = 512;
+constexpr uint32_t kHeavyThreads = 512;
+
+// Range histogram: 16-bit-style log-scale keys of the 64-bit support
+// (exact below 256; 8 mantissa bits above), weighted by the static wedge work.
+constexpr uint32_t kBins = 14336;
+__host__ __device__ __forceinline__ uint32_t support_key(uint64_t s) {
+  if (s < 256) return (uint32_t)s;
+#ifdef __CUDA_ARCH__
+  uint32_t e = 63 - __clzll((long long)s);
+#else
+  uint32_t e = 63 - __builtin_clzll(s);
+#endif
+  return 256 + (e - 8) * 256 + (uint32_t)((s >> (e - 8)) & 255);
+}
+// smallest support value mapped to key b (b <= kBins)
+__host__ __device__ __forceinline__ uint64_t key_lo(uint32_t b) {
+  if (b < 256) return b;
+  uint32_t q = (b - 256) / 256, mnt = (b - 256) % 256, e = q + 8;
+  if (e >= 64) return ~0ull;
+  return ((uint64_t)(256 + mnt)) << (e - 8);
+}
+
+struct Counters {
+  // reset every CD iteration
+  uint32_t nF;                   // frontier size (select)
+  uint32_t ntier[3];             // tier list sizes (classify)
+  unsigned long long wedges;     // Σ wl over classified work (traversal, incl. u' = u)
+  unsigned long long sel_wc;     // Σ wc over selected (range-target adaptation)
+  // managed by the host loop
+  uint32_t ntouched;             // touched V vertices (classify, CD)
+  uint32_t pad0;
+  unsigned long long live_wc;    // range pass: Σ wc over live
+  unsigned long long live_n;     // range pass: live count
+  // cumulative
+  unsigned long long updates;    // C(w,2) decrements
+  unsigned long long ld2_drop;   // compaction: decrease of Σ_v ld_v^2
+  unsigned long long cum_wedges; // Σ of every classify's wedges
+};
+
+// ---------------------------------------------------------------- init
+// live degree of every v, and Σ_v d_v^2 (one-sided re-count cost, g10)
+__global__ void k_init_v(uint32_t nV, const uint64_t* __restrict__ offV, uint32_t* __restrict__ ld,
+                         unsigned long long* sum_d2) {
+  unsigned long long acc = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nV; v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t d = (uint32_t)(offV[v + 1] - offV[v]);
+    ld[v] = d;
+    acc += (unsigned long long)d * d;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && acc) atomicAdd(sum_d2, acc);
+}
+
+// wc[u] = Σ_{v ∈ N_u} d_v : static wedge work of peeling u (proxy 2; g5)
+__global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
+                         const uint64_t* __restrict__ offV, uint64_t* __restrict__ wc,
+                         uint32_t* __restrict__ part) {
+  const uint32_t ln = lane_id();
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t u = gw; u < nU; u += nw) {
+    uint64_t s = 0;
+    for (uint64_t e = offU[u] + ln; e < offU[u + 1]; e += 32) {
+      uint32_t v = adjU[e];
+      s += offV[v + 1] - offV[v];
+    }
+    s = warp_sum(s);
+    if (ln == 0) {
+      wc[u] = s;
+      part[u] = kUnassigned;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- classify
+// For each listed u (or every unassigned u when list == nullptr) compute
+// wl = Σ_{v∈N_u} ld[v] (wedges its traversal reads) and route it to a tier by
+// the partner bound pb = wl - d_u.  Vertices that cannot decrement anybody
+// (d_u < 2, pb == 0, or — peeling — exact support 0) are not traversed; in
+// COUNT mode their support is written as 0 here.  Optionally marks every
+// v ∈ N_u as touched (epoch tag) for the deletion pass.
+template <int MODE>
+__global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
+                           const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
+                           const uint32_t* __restrict__ ld, const uint32_t* __restrict__ part,
+                           uint64_t* __restrict__ support, uint2* tier0, uint2* tier1, uint2* tier2,
+                           uint32_t* vflag, uint32_t epoch, uint32_t* touched, Counters* c) {
+  const uint32_t ln = lane_id();
+  const uint32_t n = list ? *count : nU;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long wsum = 0;
+  for (uint64_t b = gw * 32; b < n; b += nw * 32) {
+    uint32_t my_u = 0;
+    uint64_t my_wl = 0;
+    bool my_ok = false;
+    const uint32_t cnt = (uint32_t)(n - b < 32 ? n - b : 32);
+    for (uint32_t k = 0; k < cnt; k++) {
+      const uint32_t u = list ? list[b + k] : (uint32_t)(b + k);
+      if (!list && part[u] != kUnassigned) continue;  // warp-uniform
+      uint64_t s = 0;
+      const uint64_t e0 = offU[u], e1 = offU[u + 1];
+      for (uint64_t eb = e0; eb < e1; eb += 32) {  // warp-uniform trip count
+        const uint64_t e = eb + ln;
+        bool fresh = false;
+        uint32_t v = 0;
+        if (e < e1) {
+          v = adjU[e];
+          s += ld[v];
+          if (vflag && vflag[v] != epoch) fresh = atomicExch(&vflag[v], epoch) != epoch;
+        }
+        if (vflag) warp_append(fresh, v, touched, &c->ntouched);
+      }
+      s = warp_sum(s);
+      if (ln == k) {
+        my_u = u;
+        my_wl = s;
+        my_ok = true;
+      }
+    }
+    int tier = -1;
+    uint32_t pb = 0;
+    if (my_ok) {
+      const uint64_t d = offU[my_u + 1] - offU[my_u];
+      const uint64_t pb64 = my_wl - d;
+      bool work = d >= 2 && pb64 > 0;
+      if (MODE == 1 && work) work = support[my_u] != 0;
+      if (work) {
+        pb = pb64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb64;
+        tier = pb <= kWarpCap ? 0 : (pb <= kCtaCap ? 1 : 2);
+        wsum += my_wl;
+      } else if (MODE == 0) {
+        support[my_u] = 0;
+      }
+    }
+    const uint2 item = make_uint2(my_u, pb);
+    warp_append2(tier == 0, item, tier0, &c->ntier[0]);
+    warp_append2(tier == 1, item, tier1, &c->ntier[1]);
+    warp_append2(tier == 2, item, tier2, &c->ntier[2]);
+  }
+  wsum = warp_sum(wsum);
+  if (ln == 0 && wsum) {
+    atomicAdd(&c->wedges, wsum);
+    atomicAdd(&c->cum_wedges, wsum);
+  }
+}
+
+// ---------------------------------------------------------------- aggregation
+// MODE 0 (COUNT): support[u] = Σ_{u' unassigned, u' != u} C(w(u,u'),2)
+// MODE 1 (PEEL):  for u in the frontier, every unassigned u' with w >= 2:
+//                 support[u'] -= C(w(u,u'),2)   (tip batch update, P:987-991:
+//                 updates from different frontier vertices touch disjoint
+//                 butterflies, so they are summed atomically; no floor needed)
+struct AggArgs {
+  const uint64_t* __restrict__ offU;
+  const uint32_t* __restrict__ adjU;
+  const uint64_t* __restrict__ offV;
+  const uint32_t* __restrict__ adjV;  // live adjacency (prefix ld[v] of each list)
+  const uint32_t* __restrict__ ld;
+  const uint32_t* __restrict__ part;
+  uint64_t* support;
+  const uint2* __restrict__ list;
+  const uint32_t* __restrict__ count;
+  uint32_t* slot_cnt;    // heavy tier: per slot dense counters [nU]
+  uint32_t* slot_touch;  // heavy tier: per slot first-touch list [nU]
+  uint32_t* slot_dup;    // heavy tier: per slot w>=2 list [nU]
+  uint32_t nU;
+  Counters* c;
+};
+
+template <int MODE>
+__device__ __forceinline__ void emit(const AggArgs& a, uint32_t k, uint32_t w, uint64_t& acc, unsigned long long& upd) {
+  if (w >= 2 && a.part[k] == kUnassigned) {
+    const uint64_t d = choose2(w);
+    if (MODE == 0) {
+      acc += d;
+    } else {
+      red_add_u64(&a.support[k], 0ull - d);
+      upd++;
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t w = threadIdx.x >> 5, ln = lane_id();
+  uint32_t* keys = sm + w * (2 * kWarpSlots);
+  uint32_t* vals = keys + kWarpSlots;
+  for (uint32_t s = ln; s < kWarpSlots; s += 32) {
+    keys[s] = kEmpty;
+    vals[s] = 0;
+  }
+  __syncwarp();
+  const uint32_t n = *a.count;
+  const CdLists L{a.adjU, a.offV, a.ld};
+  unsigned long long upd = 0;
+  const uint32_t wpb = blockDim.x >> 5;
+  for (uint32_t i = blockIdx.x * wpb + w; i < n; i += gridDim.x * wpb) {
+    const uint2 it = a.list[i];
+    const uint32_t u = it.x;
+    uint32_t logT = ceil_log2(2 * it.y);
+    logT = logT < 5 ? 5 : logT;
+    auto f = [&](bool ok, uint32_t x) {
+      if (ok && x != u) hash_insert(keys, vals, logT, x);
+    };
+    warp_wedges(L, a.offU[u], a.offU[u + 1], a.adjV, f);
+    __syncwarp();
+    uint64_t acc = 0;
+    const uint32_t T = 1u << logT;
+    for (uint32_t s = ln; s < T; s += 32) {
+      const uint32_t k = keys[s];
+      if (k != kEmpty) {
+        const uint32_t wv = vals[s];
+        keys[s] = kEmpty;
+        vals[s] = 0;
+        emit<MODE>(a, k, wv, acc, upd);
+      }
+    }
+    if (MODE == 0) {
+      acc = warp_sum(acc);
+      if (ln == 0) a.support[u] = acc;
+    }
+    __syncwarp();
+  }
+  if (MODE == 1) {
+    upd = warp_sum(upd);
+    if (ln == 0 && upd) atomicAdd(&a.c->updates, upd);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kCtaTierThreads) k_agg_cta(AggArgs a) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* keys = sm;
+  uint32_t* vals = sm + kCtaSlots;
+  uint32_t* s_long = vals + kCtaSlots;              // blockDim entries
+  uint32_t* s_misc = s_long + kCtaTierThreads;      // [0] nlong, [1..34] scan
+  __shared__ unsigned long long s_acc;
+  for (uint32_t s = threadIdx.x; s < kCtaSlots; s += blockDim.x) {
+    keys[s] = kEmpty;
+    vals[s] = 0;
+  }
+  __syncthreads();
+  const uint32_t n = *a.count;
+  const CdLists L{a.adjU, a.offV, a.ld};
+  unsigned long long upd = 0;
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint2 it = a.list[i];
+    const uint32_t u = it.x;
+    uint32_t logT = ceil_log2(2 * it.y);
+    logT = logT < 5 ? 5 : (logT > 14 ? 14 : logT);
+    if (threadIdx.x == 0) s_acc = 0;
+    auto f = [&](bool ok, uint32_t x) {
+      if (ok && x != u) hash_insert(keys, vals, logT, x);
+    };
+    cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjV, s_long, s_misc, f);
+    uint64_t acc = 0;
+    const uint32_t T = 1u << logT;
+    for (uint32_t s = threadIdx.x; s < T; s += blockDim.x) {
+      const uint32_t k = keys[s];
+      if (k != kEmpty) {
+        const uint32_t wv = vals[s];
+        keys[s] = kEmpty;
+        vals[s] = 0;
+        emit<MODE>(a, k, wv, acc, upd);
+      }
+    }
+    if (MODE == 0) {
+      acc = warp_sum(acc);
+      if (lane_id() == 0 && acc) atomicAdd(&s_acc, (unsigned long long)acc);
+      __syncthreads();
+      if (threadIdx.x == 0) a.support[u] = s_acc;
+    }
+    __syncthreads();
+  }
+  if (MODE == 1) {
+    upd = warp_sum(upd);
+    if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
+  }
+}
+
+// Heavy tier: partners exceed the CTA table.  Each CTA owns a slot of dense
+// global counters over U (the paper's private n-element wedge_count array,
+// P:388-390, space term n·T of P:1419-1424); first touches and w>=2 events
+// are appended to per-slot lists so emission and reset cost O(distinct).
+template <int MODE>
+__global__ void __launch_bounds__(kHeavyThreads) k_agg_heavy(AggArgs a) {
+  __shared__ uint32_t s_long[kHeavyThreads];
+  __shared__ uint32_t s_nlong;
+  __shared__ uint32_t s_ntouch, s_ndup;
+  __shared__ unsigned long long s_acc;
+  uint32_t* cnt = a.slot_cnt + (uint64_t)blockIdx.x * a.nU;
+  uint32_t* touch = a.slot_touch + (uint64_t)blockIdx.x * a.nU;
+  uint32_t* dup = a.slot_dup + (uint64_t)blockIdx.x * a.nU;
+  const uint32_t n = *a.count;
+  const CdLists L{a.adjU, a.offV, a.ld};
+  unsigned long long upd = 0;
+  const uint32_t ln = lane_id();
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t u = a.list[i].x;
+    if (threadIdx.x == 0) {
+      s_ntouch = 0;
+      s_ndup = 0;
+      s_acc = 0;
+    }
+    __syncthreads();
+    auto f = [&](bool ok, uint32_t x) {
+      bool first = false, second = false;
+      if (ok && x != u) {
+        const uint32_t old = atomicAdd(&cnt[x], 1u);
+        first = old == 0;
+        second = old == 1;
+      }
+      uint32_t m = __ballot_sync(kFull, first);
+      if (m) {
+        uint32_t base = 0;
+        const uint32_t leader = __ffs(m) - 1;
+        if (ln == leader) base = atomicAdd(&s_ntouch, (uint32_t)__popc(m));
+        base = __shfl_sync(kFull, base, leader);
+        if (first) touch[base + __popc(m & lanemask_lt())] = x;
+      }
+      m = __ballot_sync(kFull, second);
+      if (m) {
+        uint32_t base = 0;
+        const uint32_t leader = __ffs(m) - 1;
+        if (ln == leader) base = atomicAdd(&s_ndup, (uint32_t)__popc(m));
+        base = __shfl_sync(kFull, base, leader);
+        if (second) dup[base + __popc(m & lanemask_lt())] = x;
+      }
+    };
+    cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjV, s_long, &s_nlong, f);
+    const uint32_t nd = s_ndup, nt = s_ntouch;
+    uint64_t acc = 0;
+    for (uint32_t j = threadIdx.x; j < nd; j += blockDim.x) {
+      const uint32_t k = dup[j];
+      emit<MODE>(a, k, cnt[k], acc, upd);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < nt; j += blockDim.x) cnt[touch[j]] = 0;
+    if (MODE == 0) {
+      acc = warp_sum(acc);
+      if (ln == 0 && acc) atomicAdd(&s_acc, (unsigned long long)acc);
+    }
+    __syncthreads();
+    if (MODE == 0 && threadIdx.x == 0) a.support[u] = s_acc;
+  }
+  if (MODE == 1) {
+    upd = warp_sum(upd);
+    if (ln == 0 && upd) atomicAdd(&a.c->updates, upd);
+  }
+}
+
+// ---------------------------------------------------------------- range pass
+// Partition start (Alg.4 l.5-8): snapshot ⋈^init = support for all
+// live u and build the wedge-work-weighted histogram of current supports
+// (find_range bins; tip bins keyed by support P:1387-1391).
+__global__ void __launch_bounds__(1024) k_range_hist(uint32_t nU, const uint32_t* __restrict__ part,
+                                                     const uint64_t* __restrict__ support,
+                                                     const uint64_t* __restrict__ wc, uint64_t* __restrict__ init,
+                                                     unsigned long long* ghist_w, uint32_t* ghist_n, Counters* c) {
+  extern __shared__ unsigned long long hsm[];
+  unsigned long long* hw = hsm;
+  uint32_t* hn = (uint32_t*)(hsm + kBins);
+  for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x) {
+    hw[b] = 0;
+    hn[b] = 0;
+  }
+  __syncthreads();
+  unsigned long long tw = 0, tn = 0;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nU; u += (uint64_t)gridDim.x * blockDim.x) {
+    if (part[u] != kUnassigned) continue;
+    const uint64_t s = support[u];
+    init[u] = s;
+    const uint32_t k = support_key(s);
+    const uint64_t w = wc[u];
+    if (w) atomicAdd(&hw[k], (unsigned long long)w);
+    atomicAdd(&hn[k], 1u);
+    tw += w;
+    tn++;
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x) {
+    if (hn[b]) {
+      atomicAdd(&ghist_n[b], hn[b]);
+      if (hw[b]) atomicAdd(&ghist_w[b], hw[b]);
+    }
+  }
+  tw = warp_sum(tw);
+  tn = warp_sum(tn);
+  if (lane_id() == 0 && tn) {
+    atomicAdd(&c->live_wc, tw);
+    atomicAdd(&c->live_n, tn);
+  }
+}
+
+// ---------------------------------------------------------------- frontier
+// activeSet = { live u : support[u] < bound }  (Alg.4 l.9/l.13),
+// assigned to partition pid.  Warp ballots + block-wide scan give one global
+// atomic per CTA tile for the compacted list.
+__global__ void __launch_bounds__(256) k_select(uint32_t nU, uint32_t* __restrict__ part,
+                                                const uint64_t* __restrict__ support,
+                                                const uint64_t* __restrict__ wc, uint64_t bound, uint32_t pid,
+                                                uint32_t* __restrict__ F, Counters* c) {
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_base;
+  unsigned long long swc = 0;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < nU; b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = b + threadIdx.x;
+    bool sel = false;
+    if (u < nU && part[u] == kUnassigned && support[u] < bound) sel = true;
+    uint32_t total;
+    const uint32_t r = block_excl_scan(sel ? 1u : 0u, s_scan, &total);
+    if (total) {
+      if (threadIdx.x == 0) s_base = atomicAdd(&c->nF, total);
+      __syncthreads();
+      if (sel) {
+        F[s_base + r] = (uint32_t)u;
+        part[u] = pid;
+        swc += wc[u];
+      }
+      __syncthreads();
+    }
+  }
+  swc = warp_sum(swc);
+  if (lane_id() == 0 && swc) atomicAdd(&c->sel_wc, swc);
+}
+
+// ---------------------------------------------------------------- deletion
+// Dynamic graph update: for every touched v, stable-partition
+// the live prefix of N_v into [still live | newly peeled]; the peeled block is
+// placed directly after the live prefix, so over the whole CD each N_v ends as
+// [U_last | ... | U_1] — grouped by partition, which is the induced-subgraph
+// layout FD needs.  Lists shorter than `big` use one warp,
+// longer ones one CTA (k_compact_big).
+__global__ void k_compact(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv,
+                          const uint64_t* __restrict__ offV, uint32_t* adjL, uint32_t* tmp, uint32_t* ld,
+                          const uint32_t* __restrict__ part, uint32_t big, Counters* c) {
+  const uint32_t ln = lane_id();
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t n = *ntv;
+  unsigned long long drop = 0;
+  for (uint64_t i = gw; i < n; i += nw) {
+    const uint32_t v = tv[i];
+    const uint32_t L = ld[v];
+    if (L >= big) continue;
+    const uint64_t base = offV[v];
+    for (uint32_t t = ln; t < L; t += 32) tmp[base + t] = adjL[base + t];
+    __syncwarp();
+    uint32_t lw = 0, dw = 0;
+    for (uint32_t t0 = 0; t0 < L; t0 += 32) {
+      const uint32_t t = t0 + ln;
+      const bool ok = t < L;
+      const uint32_t x = ok ? tmp[base + t] : 0u;
+      const bool live = ok && part[x] == kUnassigned;
+      const bool dead = ok && !live;
+      const uint32_t ml = __ballot_sync(kFull, live), md = __ballot_sync(kFull, dead);
+      if (live) adjL[base + lw + __popc(ml & lanemask_lt())] = x;
+      if (dead) adjL[base + L - 1 - (dw + __popc(md & lanemask_lt()))] = x;
+      lw += __popc(ml);
+      dw += __popc(md);
+    }
+    if (ln == 0) {
+      ld[v] = lw;
+      drop += (unsigned long long)L * L - (unsigned long long)lw * lw;
+    }
+    __syncwarp();
+  }
+  drop = warp_sum(drop);
+  if (ln == 0 && drop) atomicAdd(&c->ld2_drop, drop);
+}
+
+__global__ void __launch_bounds__(512) k_compact_big(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv,
+                                                     const uint64_t* __restrict__ offV, uint32_t* adjL, uint32_t* tmp,
+                                                     uint32_t* ld, const uint32_t* __restrict__ part, uint32_t big,
+                                                     Counters* c) {
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_L;
+  const uint32_t n = *ntv;
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t v = tv[i];
+    if (threadIdx.x == 0) s_L = ld[v];
+    __syncthreads();
+    const uint32_t L = s_L;
+    if (L < big) {
+      __syncthreads();
+      continue;
+    }
+    const uint64_t base = offV[v];
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) tmp[base + t] = adjL[base + t];
+    __syncthreads();
+    uint32_t lw = 0, dw = 0;
+    for (uint32_t t0 = 0; t0 < L; t0 += blockDim.x) {
+      const uint32_t t = t0 + threadIdx.x;
+      const bool ok = t < L;
+      const uint32_t x = ok ? tmp[base + t] : 0u;
+      const bool live = ok && part[x] == kUnassigned;
+      const bool dead = ok && !live;
+      uint32_t tl, td;
+      const uint32_t rl = block_excl_scan(live ? 1u : 0u, s_scan, &tl);
+      const uint32_t rd = block_excl_scan(dead ? 1u : 0u, s_scan, &td);
+      if (live) adjL[base + lw + rl] = x;
+      if (dead) adjL[base + L - 1 - (dw + rd)] = x;
+      lw += tl;
+      dw += td;
+    }
+    if (threadIdx.x == 0) {
+      ld[v] = lw;
+      atomicAdd(&c->ld2_drop, (unsigned long long)L * L - (unsigned long long)lw * lw);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- validation
+// PBNG_OPT_VALIDATE: offsets[0]=0, monotone, offsets[n]=m, indices < n_other.
+__global__ void k_validate_csr(uint32_t n, uint64_t m, const uint64_t* __restrict__ off,
+                               const uint32_t* __restrict__ idx, uint32_t n_other, uint32_t* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n + 1 || i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i <= n) {
+      const uint64_t o = off[i];
+      if ((i == 0 && o != 0) || (i == n && o != m) || (i < n && off[i + 1] < o) || o > m) atomicOr(bad, 1u);
+    }
+    if (i < m && idx[i] >= n_other) atomicOr(bad, 2u);
+  }
+}
+
+}  // namespace pbng

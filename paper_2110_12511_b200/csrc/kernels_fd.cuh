@@ -1,0 +1,324 @@
+// kernels_fd.cuh — fine-grained decomposition (FD) kernels.
+//
+// Paper: arXiv 2110.12511 ("P:n" = PAPER.md line).
+//   FD principle: peel each partition independently from ⋈^init
+//   tip FD on the induced subgraph G_i = (U_i, V), edge in exactly one
+//   LPT work estimate = wedges of G_i with both endpoints in U_i
+//   dynamic task allocation (threads pop partition ids)
+// Each partition is peeled level-synchronously inside one CTA: the level
+// k = max(k, min live support); every live vertex with support <= k gets
+// θ = k and is peeled in the same round (equal to sequential BUP on G_i,
+// Alg.2 P:508-531 with the max(θ, ·) floor; exact supports need no clamp).
+#pragma once
+#include "kernels_cd.cuh"
+
+namespace pbng {
+
+constexpr uint32_t kFdThreads = 512;
+constexpr uint32_t kFdWarpSlots = 512;
+constexpr uint32_t kFdWarpCap = kFdWarpSlots / 2;
+
+// ---------------------------------------------------------------- membership
+__global__ void k_part_count(uint32_t nU, const uint32_t* __restrict__ part, uint32_t nparts, uint32_t* pcount) {
+  extern __shared__ uint32_t hc[];
+  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x) hc[i] = 0;
+  __syncthreads();
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nU; u += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hc[part[u]], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x)
+    if (hc[i]) atomicAdd(&pcount[i], hc[i]);
+}
+
+// members grouped by partition: members[poff[p] ..) (order inside a group is free)
+__global__ void k_part_scatter(uint32_t nU, const uint32_t* __restrict__ part, const uint32_t* __restrict__ poff,
+                               uint32_t* pcur, uint32_t* members) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < nU; b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = b + threadIdx.x;
+    const bool ok = u < nU;
+    const uint32_t p = ok ? part[u] : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(kFull, p);
+    if (ok) {
+      const uint32_t leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (lane_id() == leader) base = atomicAdd(&pcur[p], (uint32_t)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      members[poff[p] + base + __popc(peers & lanemask_lt())] = (uint32_t)u;
+    }
+  }
+}
+
+// first index i in [0, n) of a list sorted by part descending with
+// part[list[i]] <= p (strict: < p); n if none.
+__device__ __forceinline__ uint32_t desc_bound(const uint32_t* __restrict__ list, uint32_t n,
+                                               const uint32_t* __restrict__ part, uint32_t p, bool strict) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint32_t q = part[list[mid]];
+    if (strict ? q < p : q <= p) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// For every U-edge (u, v): the segment N_v ∩ U_part[u] of the partition-ordered
+// list (seg = lo | hi << 32), and the LPT work estimate
+// work[p] = Σ_{u∈U_p} Σ_{v∈N_u} |N_v ∩ U_p| = Σ_v |N_v ∩ U_p|^2  (g13).
+__global__ void k_fd_seg(uint32_t nU, const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
+                         const uint64_t* __restrict__ offV, const uint32_t* __restrict__ adjL,
+                         const uint32_t* __restrict__ part, uint32_t nparts, uint64_t* __restrict__ seg,
+                         unsigned long long* work) {
+  extern __shared__ unsigned long long sw[];
+  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x) sw[i] = 0;
+  __syncthreads();
+  const uint32_t ln = lane_id();
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t u = gw; u < nU; u += nw) {
+    const uint32_t p = part[u];
+    unsigned long long acc = 0;
+    for (uint64_t e = offU[u] + ln; e < offU[u + 1]; e += 32) {
+      const uint32_t v = adjU[e];
+      const uint64_t b = offV[v];
+      const uint32_t n = (uint32_t)(offV[v + 1] - b);
+      const uint32_t lo = desc_bound(adjL + b, n, part, p, false);
+      const uint32_t hi = desc_bound(adjL + b, n, part, p, true);
+      seg[e] = (uint64_t)lo | ((uint64_t)hi << 32);
+      acc += hi - lo;
+    }
+    acc = warp_sum(acc);
+    if (ln == 0 && acc) atomicAdd(&sw[p], acc);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x)
+    if (sw[i]) atomicAdd(&work[i], sw[i]);
+}
+
+// ---------------------------------------------------------------- FD peel
+struct FdArgs {
+  uint32_t nU;
+  const uint64_t* __restrict__ offU;
+  const uint32_t* __restrict__ adjU;
+  const uint64_t* __restrict__ offV;
+  const uint32_t* __restrict__ adjL;
+  const uint64_t* __restrict__ seg;
+  const uint32_t* __restrict__ poff;
+  const uint32_t* __restrict__ order;  // partition ids, decreasing work (LPT)
+  uint32_t nparts;
+  uint32_t* ticket;
+  uint32_t* members;  // live list per partition (compacted in place)
+  uint32_t* sel;      // vertices peeled this round
+  uint32_t* selpb;    // partner bound per selected vertex (0 = nothing to update)
+  uint64_t* s;        // FD supports, initialised to ⋈^init
+  uint8_t* peeled;
+  uint64_t* theta;
+  uint32_t* slot_cnt;
+  uint32_t* slot_touch;
+  uint32_t* slot_dup;
+  unsigned long long* wedges;
+  unsigned long long* updates;
+  uint32_t* rounds_max;
+};
+
+__device__ __forceinline__ void fd_emit(const FdArgs& a, uint32_t k, uint32_t w, unsigned long long& upd) {
+  if (w >= 2 && !a.peeled[k]) {
+    red_add_u64(&a.s[k], 0ull - choose2(w));
+    upd++;
+  }
+}
+
+__global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t w = threadIdx.x >> 5, ln = lane_id(), nw = blockDim.x >> 5;
+  uint32_t* wkeys = sm + w * (2 * kFdWarpSlots);
+  uint32_t* wvals = wkeys + kFdWarpSlots;
+  uint32_t* ckeys = sm + nw * (2 * kFdWarpSlots);
+  uint32_t* cvals = ckeys + kCtaSlots;
+  uint32_t* s_long = cvals + kCtaSlots;
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t;
+  __shared__ unsigned long long s_min;
+  for (uint32_t i = threadIdx.x; i < nw * 2 * kFdWarpSlots; i += blockDim.x) sm[i] = (i / kFdWarpSlots) % 2 == 0 ? kEmpty : 0u;
+  for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) {
+    ckeys[i] = kEmpty;
+    cvals[i] = 0;
+  }
+  uint32_t* hcnt = a.slot_cnt + (uint64_t)blockIdx.x * a.nU;
+  uint32_t* htouch = a.slot_touch + (uint64_t)blockIdx.x * a.nU;
+  uint32_t* hdup = a.slot_dup + (uint64_t)blockIdx.x * a.nU;
+  const FdLists L{a.adjU, a.offV, a.seg};
+  unsigned long long wedges = 0, upd = 0;
+  uint32_t rounds_max = 0;
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) s_t = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const uint32_t t = s_t;
+    __syncthreads();
+    if (t >= a.nparts) break;
+    const uint32_t p = a.order[t];
+    const uint32_t lo = a.poff[p];
+    uint32_t live = a.poff[p + 1] - lo;
+    uint64_t k = 0;
+    uint32_t rounds = 0;
+    while (live > 0) {
+      // (1) level k = max(k, min live support)
+      if (threadIdx.x == 0) s_min = ~0ull;
+      __syncthreads();
+      uint64_t mn = ~0ull;
+      for (uint32_t j = threadIdx.x; j < live; j += blockDim.x) {
+        const uint64_t v = a.s[a.members[lo + j]];
+        mn = v < mn ? v : mn;
+      }
+      mn = warp_min_u64(mn);
+      if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
+      __syncthreads();
+      k = s_min > k ? s_min : k;
+      // (2) select {support <= k}: θ = k; compact the rest in place
+      uint32_t nsel = 0, nkeep = 0;
+      for (uint32_t c0 = 0; c0 < live; c0 += blockDim.x) {
+        const uint32_t j = c0 + threadIdx.x;
+        const bool ok = j < live;
+        const uint32_t u = ok ? a.members[lo + j] : 0u;
+        const bool sl = ok && a.s[u] <= k;
+        const bool kp = ok && !sl;
+        uint32_t ts, tk;
+        const uint32_t rs = block_excl_scan(sl ? 1u : 0u, s_scan, &ts);
+        const uint32_t rk = block_excl_scan(kp ? 1u : 0u, s_scan, &tk);
+        if (sl) {
+          a.sel[lo + nsel + rs] = u;
+          a.theta[u] = k;
+          a.peeled[u] = 1;
+        }
+        if (kp) a.members[lo + nkeep + rk] = u;
+        nsel += ts;
+        nkeep += tk;
+      }
+      live = nkeep;
+      rounds++;
+      __syncthreads();
+      // (3) partner bound of each selected vertex inside G_p
+      for (uint32_t j = w; j < nsel; j += nw) {
+        const uint32_t u = a.sel[lo + j];
+        const uint64_t e0 = a.offU[u], e1 = a.offU[u + 1];
+        uint64_t wl = 0;
+        for (uint64_t e = e0 + ln; e < e1; e += 32) {
+          uint64_t b;
+          uint32_t len;
+          L.get(e, b, len);
+          wl += len;
+        }
+        wl = warp_sum(wl);
+        if (ln == 0) {
+          const uint64_t d = e1 - e0;
+          const uint64_t pb = wl - d;  // u appears once in each of its segments
+          uint32_t r = 0;
+          if (d >= 2 && pb > 0 && a.s[u] != 0) {
+            r = pb > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb;
+            wedges += wl;
+          }
+          a.selpb[lo + j] = r;
+        }
+      }
+      __syncthreads();
+      // (4) light: one warp per vertex, per-warp table
+      for (uint32_t j = w; j < nsel; j += nw) {
+        const uint32_t pb = a.selpb[lo + j];
+        if (pb == 0 || pb > kFdWarpCap) continue;
+        const uint32_t u = a.sel[lo + j];
+        uint32_t logT = ceil_log2(2 * pb);
+        logT = logT < 5 ? 5 : logT;
+        auto f = [&](bool ok, uint32_t x) {
+          if (ok && x != u) hash_insert(wkeys, wvals, logT, x);
+        };
+        warp_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, f);
+        __syncwarp();
+        for (uint32_t s = ln; s < (1u << logT); s += 32) {
+          const uint32_t key = wkeys[s];
+          if (key != kEmpty) {
+            const uint32_t wv = wvals[s];
+            wkeys[s] = kEmpty;
+            wvals[s] = 0;
+            fd_emit(a, key, wv, upd);
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      // (5) medium / heavy: whole CTA per vertex
+      for (uint32_t j = 0; j < nsel; j++) {
+        const uint32_t pb = a.selpb[lo + j];
+        if (pb <= kFdWarpCap) continue;  // uniform
+        const uint32_t u = a.sel[lo + j];
+        if (pb <= kCtaCap) {
+          uint32_t logT = ceil_log2(2 * pb);
+          logT = logT > 14 ? 14 : logT;
+          auto f = [&](bool ok, uint32_t x) {
+            if (ok && x != u) hash_insert(ckeys, cvals, logT, x);
+          };
+          cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_long, &s_nlong, f);
+          for (uint32_t s = threadIdx.x; s < (1u << logT); s += blockDim.x) {
+            const uint32_t key = ckeys[s];
+            if (key != kEmpty) {
+              const uint32_t wv = cvals[s];
+              ckeys[s] = kEmpty;
+              cvals[s] = 0;
+              fd_emit(a, key, wv, upd);
+            }
+          }
+          __syncthreads();
+        } else {
+          if (threadIdx.x == 0) {
+            s_ntouch = 0;
+            s_ndup = 0;
+          }
+          __syncthreads();
+          auto f = [&](bool ok, uint32_t x) {
+            bool first = false, second = false;
+            if (ok && x != u) {
+              const uint32_t old = atomicAdd(&hcnt[x], 1u);
+              first = old == 0;
+              second = old == 1;
+            }
+            uint32_t m = __ballot_sync(kFull, first);
+            if (m) {
+              uint32_t base = 0;
+              const uint32_t leader = __ffs(m) - 1;
+              if (ln == leader) base = atomicAdd(&s_ntouch, (uint32_t)__popc(m));
+              base = __shfl_sync(kFull, base, leader);
+              if (first) htouch[base + __popc(m & lanemask_lt())] = x;
+            }
+            m = __ballot_sync(kFull, second);
+            if (m) {
+              uint32_t base = 0;
+              const uint32_t leader = __ffs(m) - 1;
+              if (ln == leader) base = atomicAdd(&s_ndup, (uint32_t)__popc(m));
+              base = __shfl_sync(kFull, base, leader);
+              if (second) hdup[base + __popc(m & lanemask_lt())] = x;
+            }
+          };
+          cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_long, &s_nlong, f);
+          const uint32_t nd = s_ndup, nt = s_ntouch;
+          for (uint32_t q = threadIdx.x; q < nd; q += blockDim.x) {
+            const uint32_t key = hdup[q];
+            fd_emit(a, key, hcnt[key], upd);
+          }
+          __syncthreads();
+          for (uint32_t q = threadIdx.x; q < nt; q += blockDim.x) hcnt[htouch[q]] = 0;
+          __syncthreads();
+        }
+      }
+      __syncthreads();
+    }
+    rounds_max = rounds > rounds_max ? rounds : rounds_max;
+  }
+  wedges = warp_sum(wedges);
+  upd = warp_sum(upd);
+  if (ln == 0) {
+    if (wedges) atomicAdd(a.wedges, wedges);
+    if (upd) atomicAdd(a.updates, upd);
+  }
+  if (threadIdx.x == 0) atomicMax(a.rounds_max, rounds_max);
+}
+
+}  // namespace pbng

@@ -1,0 +1,173 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+All integer outputs must match bit for bit (uint64 butterfly counts and tip
+numbers); the partition plan is heuristic and is checked by the invariants the
+paper's lemmas give (Lemmas 3-4; ⋈^init).
+"""
+import numpy as np
+import pytest
+
+import graphgen as gg
+import oracle
+from oracle import brute
+
+pytestmark = pytest.mark.gpu
+
+KINF = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+@pytest.fixture(scope="module")
+def pb(cuda_ok):
+    import __graft_entry__ as entry
+    entry.build()
+    import paper_2110_12511_b200 as pbng
+    return pbng
+
+
+def dev(pb, g):
+    return pb.DeviceGraph.from_numpy(g.off_u, g.adj_u, g.off_v, g.adj_v)
+
+
+def tiny_corpus(n, seed0):
+    rng = np.random.default_rng(seed0)
+    for i in range(n):
+        nu = int(rng.integers(1, 14))
+        nv = int(rng.integers(1, 14))
+        m = int(rng.integers(0, nu * nv + 1))
+        yield gg.uniform(nu, nv, m, seed=seed0 + i)
+
+
+def test_count_tiny_corpus(pb):
+    for g in tiny_corpus(150, 100):
+        d = dev(pb, g)
+        assert np.array_equal(pb.as_u64(pb.pbng_count_butterflies(d, side=0)), oracle.count(g))
+        assert np.array_equal(pb.as_u64(pb.pbng_count_butterflies(d, side=1)), oracle.count(g.swapped()))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, "2a"])
+def test_count_configs(pb, cfg):
+    g, _ = gg.config(cfg)
+    assert np.array_equal(pb.as_u64(pb.pbng_count_butterflies(dev(pb, g))), oracle.count(g))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_tip_tiny_corpus(pb, P):
+    for g in tiny_corpus(120, 1000 + P):
+        d = dev(pb, g)
+        for side, gs in ((0, g), (1, g.swapped())):
+            tip, _ = pb.pbng_tip_decompose(d, P, side=side)
+            assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs)), (g.name, side, P)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, "2a"])
+@pytest.mark.parametrize("opts", [0, 1, 2, 3, 16, 18])
+def test_tip_configs_options(pb, cfg, opts):
+    g, P = gg.config(cfg)
+    want = oracle.bup_tip(g)
+    tip, st = pb.pbng_tip_decompose(dev(pb, g), P, opts=opts)
+    assert np.array_equal(pb.as_u64(tip), want)
+    assert 1 <= st["partitions_used"] <= P
+    if opts & 16:
+        assert st["recounts"] >= 1
+
+
+@pytest.mark.parametrize("P", [1, 2, 5, 16, 64, 150, 4096])
+def test_tip_partition_count_sweep(pb, P):
+    g, _ = gg.config(1)
+    tip, st = pb.pbng_tip_decompose(dev(pb, g), P)
+    assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(g))
+    assert st["partitions_used"] <= P
+
+
+def test_config2a_closed_form(pb):
+    from math import comb
+    shapes = gg.block_sizes(200, 5, 60, seed=2)
+    want = np.concatenate([[(a - 1) * comb(b, 2)] * a for a, b in shapes]).astype(np.uint64)
+    g, P = gg.config("2a")
+    tip, _ = pb.pbng_tip_decompose(dev(pb, g), P)
+    assert np.array_equal(pb.as_u64(tip), want)
+
+
+def test_config3_parity(pb):
+    """Config 3 (500K x 200K, 5M edges, Chung-Lu γ=2.1, P=150) against the full oracle."""
+    g, P = gg.config(3)
+    d = dev(pb, g)
+    sup = pb.as_u64(pb.pbng_count_butterflies(d))
+    tip, st = pb.pbng_tip_decompose(d, P)
+    want_sup = oracle.count(g)
+    assert np.array_equal(sup, want_sup)
+    assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(g))
+    assert st["partitions_used"] > 1
+
+
+def _check_plan(g, part, init, bounds, nparts, theta):
+    part = part.cpu().numpy()
+    init = init.cpu().numpy().view(np.uint64)
+    assert 1 <= nparts
+    b = bounds[: nparts + 1]
+    assert b[0] == 0 and b[-1] == KINF
+    assert np.all(b[1:] > b[:-1])                           # strictly increasing ranges
+    assert part.min() >= 0 and part.max() < nparts
+    lo, hi = b[part], b[part + 1]
+    assert np.all(theta >= lo) and np.all(theta < hi)       # θ(i) <= θ_u < θ(i+1) (Lemmas 3-4)
+    return part, init
+
+
+def test_plan_properties_tiny(pb):
+    for g in tiny_corpus(80, 7000):
+        theta = oracle.bup_tip(g)
+        for P in (2, 4):
+            part, init, bounds, nparts = pb.pbng_tip_plan(dev(pb, g), P)
+            part, init = _check_plan(g, part, init, bounds, nparts, theta)
+            assert list(init) == brute.init_support(g, list(part))  # ⋈^init
+
+
+def test_plan_properties_config1(pb):
+    g, P = gg.config(1)
+    theta = oracle.bup_tip(g)
+    for opts in (0, 2, 16):
+        part, init, bounds, nparts = pb.pbng_tip_plan(dev(pb, g), P, opts=opts)
+        _check_plan(g, part, init, bounds, nparts, theta)
+
+
+def test_host_entry_point(pb):
+    g, P = gg.config(1)
+    tip, st = pb.pbng_tip_decompose_host(g.off_u, g.adj_u, g.off_v, g.adj_v, P)
+    assert np.array_equal(tip, oracle.bup_tip(g))
+    tipv, _ = pb.pbng_tip_decompose_host(g.off_u, g.adj_u, g.off_v, g.adj_v, P, side=1)
+    assert np.array_equal(tipv, oracle.bup_tip(g.swapped()))
+
+
+def test_edge_cases(pb):
+    # empty edge set, isolated vertices
+    g = gg.from_edges(5, 3, [])
+    tip, st = pb.pbng_tip_decompose(dev(pb, g), 4)
+    assert np.all(pb.as_u64(tip) == 0)
+    assert np.all(pb.as_u64(pb.pbng_count_butterflies(dev(pb, g))) == 0)
+    # star, complete, path
+    for g, want in ((gg.complete(1, 5), [0]), (gg.complete(4, 4), [18] * 4),
+                    (gg.from_edges(2, 2, [(0, 0), (1, 0), (1, 1)]), [0, 0])):
+        tip, _ = pb.pbng_tip_decompose(dev(pb, g), 3)
+        assert list(pb.as_u64(tip)) == want
+    # errors
+    g, _ = gg.config(1)
+    d = dev(pb, g)
+    for bad in (lambda: pb.pbng_tip_decompose(d, 0), lambda: pb.pbng_tip_decompose(d, 5000),
+                lambda: pb.pbng_tip_decompose(d, 8, side=2)):
+        with pytest.raises(pb.PbngError) as ei:
+            bad()
+        assert ei.value.code == pb.ERR_ARG
+
+
+def test_validate_rejects_bad_csr(pb):
+    import torch
+    g, _ = gg.config(1)
+    d = dev(pb, g)
+    bad_adj = d.adj_u.clone()
+    bad_adj[5] = g.nV + 7
+    d2 = pb.DeviceGraph(d.nU, d.nV, d.off_u, bad_adj, d.off_v, d.adj_v)
+    with pytest.raises(pb.PbngError) as ei:
+        pb.pbng_tip_decompose(d2, 8, opts=pb.OPT_VALIDATE)
+    assert ei.value.code == pb.ERR_GRAPH
+    tip, _ = pb.pbng_tip_decompose(d, 8, opts=pb.OPT_VALIDATE)
+    torch.cuda.synchronize()
