@@ -15,7 +15,8 @@
  *                V.offsets[V.n + 1] (uint64), V.indices[V.m] (uint32 ids in U)
  *              offsets[0] = 0, non-decreasing, offsets[n] = m; U.m == V.m;
  *              no duplicate edges; the two CSRs are transposes of each other.
- *              Adjacency order within a list is free (not required sorted).
+ *              Each adjacency list must be sorted ascending (checked by
+ *              PBNG_OPT_VALIDATE).
  *   side       0: peel U (arguments as given); 1: peel V (roles swapped).
  *              "peel side" below means U for side 0 and V for side 1
  *              (tip decomposition peels one vertex set).
@@ -67,7 +68,31 @@ typedef struct {
   uint32_t partitions_used;  /* <= P (fewer when supports run out) */
   uint32_t fd_rounds_max;    /* most level rounds any FD partition needed */
   float ms_count, ms_cd, ms_fd_build, ms_fd; /* device time per phase */
+  uint64_t uv_steps;         /* (u, v) adjacency steps of traversed vertices (all phases) */
+  uint64_t uv_steps_fd;      /* ... of which in FD */
+  uint64_t updates_fd;       /* support decrements applied in FD (included in support_updates) */
+  uint32_t launches;         /* kernels launched by this call */
+  uint32_t pad;
+  uint64_t impl[4];          /* implementation counters (tier-1 ranges, replays, -, pieces walked) */
+  /* device time per kernel family, filled only with PBNG_OPT_STATS (CUDA events
+   * recorded on `stream` around each launch): index by PBNG_K_* */
+  float ms_kernel[16];
 } pbng_stats;
+
+enum {
+  PBNG_K_INIT = 0,      /* k_init_u / k_init_v / validation */
+  PBNG_K_CLASSIFY = 1,  /* k_classify: per-vertex wedge work and tier routing */
+  PBNG_K_AGG_WARP = 2,  /* k_agg_warp: tier-0 wedge aggregation (warp per vertex) */
+  PBNG_K_AGG_CTA = 3,   /* k_agg_range: tier-1 wedge aggregation (CTA per vertex, range-partitioned hash) */
+  PBNG_K_AGG_HEAVY = 4, /* k_agg_heavy: tier-2 wedge aggregation (dense global counters) */
+  PBNG_K_SELECT = 5,    /* k_select: frontier selection + compaction */
+  PBNG_K_RANGE = 6,     /* k_range_hist: ⋈^init snapshot + range histogram */
+  PBNG_K_COMPACT = 7,   /* k_compact*: dynamic deletion */
+  PBNG_K_FD_BUILD = 8,  /* partition membership, segments, LPT work */
+  PBNG_K_FD = 9,        /* k_fd: persistent fine-grained peeling */
+  PBNG_K_COUNT_VP = 10, /* vertex-priority counting kernels (when used) */
+  PBNG_K_NUM = 16
+};
 
 enum {
   PBNG_OK = 0,

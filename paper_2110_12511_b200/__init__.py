@@ -24,11 +24,13 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpbng.so")
+LIB_PATH = os.environ.get("PBNG_LIB") or os.path.join(_HERE, "libpbng.so")
 
 OK, ERR_ARG, ERR_GRAPH, ERR_OOM, ERR_CUDA = 0, 1, 2, 3, 4
 OPT_NO_RECOUNT, OPT_NO_DELETE, OPT_VALIDATE, OPT_STATS, OPT_FORCE_RECOUNT = 1, 2, 4, 8, 16
 MAX_P = 4096
+KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_heavy", "select", "range", "compact",
+                   "fd_build", "fd", "count_vp")
 EXPORTS = ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
            "pbng_last_error", "pbng_version")
 
@@ -50,10 +52,17 @@ class Stats(ctypes.Structure):
                 ("rho_cd_iters", ctypes.c_uint32), ("recounts", ctypes.c_uint32),
                 ("partitions_used", ctypes.c_uint32), ("fd_rounds_max", ctypes.c_uint32),
                 ("ms_count", ctypes.c_float), ("ms_cd", ctypes.c_float),
-                ("ms_fd_build", ctypes.c_float), ("ms_fd", ctypes.c_float)]
+                ("ms_fd_build", ctypes.c_float), ("ms_fd", ctypes.c_float),
+                ("uv_steps", ctypes.c_uint64), ("uv_steps_fd", ctypes.c_uint64), ("updates_fd", ctypes.c_uint64),
+                ("launches", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("impl", ctypes.c_uint64 * 4),
+                ("ms_kernel", ctypes.c_float * 16)]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("pad", "ms_kernel", "impl")}
+        d["impl"] = list(self.impl)
+        d["ms_kernel"] = {name: round(float(self.ms_kernel[i]), 4) for i, name in enumerate(KERNEL_FAMILIES)
+                          if self.ms_kernel[i]}
+        return d
 
 
 _lib = None

@@ -40,5 +40,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: dict) -> str:
+    """Tuning experiments: build lib<name>.so with -D overrides (not used by the product path)."""
+    out = os.path.join(HERE, f"libpbng_{name}.so")
+    cmd = [NVCC] + FLAGS + [f"-D{k}={v}" for k, v in defines.items()] + ["-o", out] + SOURCES
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

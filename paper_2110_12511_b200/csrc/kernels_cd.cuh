@@ -17,8 +17,25 @@ constexpr uint32_t kWarpCap = kWarpSlots / 2;   // partners bound for tier 0
 constexpr uint32_t kCtaSlots = 16384;           // tier 1: one CTA per u
 constexpr uint32_t kCtaCap = kCtaSlots / 2;     // partners bound for tier 1
 constexpr uint32_t kWarpTierThreads = 256;
-constexpr uint32_t kCtaTierThreads = 512;
 constexpr uint32_t kHeavyThreads = 512;
+// tier 1: range-partitioned CTA hash (see k_agg_range)
+#ifndef PBNG_RANGE_THREADS
+#define PBNG_RANGE_THREADS 1024
+#endif
+#ifndef PBNG_RANGE_SLOTS
+#define PBNG_RANGE_SLOTS 16384
+#endif
+#ifndef PBNG_RANGE_CTAS
+#define PBNG_RANGE_CTAS 1
+#endif
+#ifndef PBNG_PIECE
+#define PBNG_PIECE 512
+#endif
+constexpr uint32_t kRangeThreads = PBNG_RANGE_THREADS;
+constexpr uint32_t kRangeSlots = PBNG_RANGE_SLOTS;  // table slots; at most half are filled per range
+constexpr uint32_t kRangeCtas = PBNG_RANGE_CTAS;    // resident CTAs per SM (overlap barrier waits)
+constexpr uint32_t kRangeLogSlots = 31 - __builtin_clz(PBNG_RANGE_SLOTS);
+constexpr uint32_t kPiece = PBNG_PIECE;             // partner lists are walked in pieces of this length
 
 // Range histogram: 16-bit-style log-scale keys of the 64-bit support
 // (exact below 256; 8 mantissa bits above), weighted by the static wedge work.
@@ -41,9 +58,10 @@ __host__ __device__ __forceinline__ uint64_t key_lo(uint32_t b) {
 }
 
 struct Counters {
-  // reset every CD iteration
+  // reset every CD iteration (host memsets [0, offsetof(ntouched)))
   uint32_t nF;                   // frontier size (select)
   uint32_t ntier[3];             // tier list sizes (classify)
+  uint32_t ticket[4];            // dynamic work tickets of the aggregation kernels
   unsigned long long wedges;     // Σ wl over classified work (traversal, incl. u' = u)
   unsigned long long sel_wc;     // Σ wc over selected (range-target adaptation)
   // managed by the host loop
@@ -55,6 +73,9 @@ struct Counters {
   unsigned long long updates;    // C(w,2) decrements
   unsigned long long ld2_drop;   // compaction: decrease of Σ_v ld_v^2
   unsigned long long cum_wedges; // Σ of every classify's wedges
+  unsigned long long cum_steps;  // Σ d_u of every traversed u ((u, v) steps)
+  unsigned long long tier_wedges[3];  // Σ wl routed to each tier
+  unsigned long long dbg[4];          // tier-1 internals: ranges, replays, steps, pieces walked
 };
 
 // ---------------------------------------------------------------- init
@@ -72,24 +93,31 @@ __global__ void k_init_v(uint32_t nV, const uint64_t* __restrict__ offV, uint32_
 }
 
 // wc[u] = Σ_{v ∈ N_u} d_v : static wedge work of peeling u (proxy 2; g5)
+// Also the most list pieces any u can have (tier-1 cursor scratch size).
 __global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                          const uint64_t* __restrict__ offV, uint64_t* __restrict__ wc,
-                         uint32_t* __restrict__ part) {
+                         uint32_t* __restrict__ part, unsigned long long* max_pieces) {
   const uint32_t ln = lane_id();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long mp = 0;
   for (uint64_t u = gw; u < nU; u += nw) {
-    uint64_t s = 0;
+    uint64_t s = 0, pc = 0;
     for (uint64_t e = offU[u] + ln; e < offU[u + 1]; e += 32) {
       uint32_t v = adjU[e];
-      s += offV[v + 1] - offV[v];
+      const uint64_t d = offV[v + 1] - offV[v];
+      s += d;
+      pc += (d + kPiece - 1) / kPiece;
     }
     s = warp_sum(s);
+    pc = warp_sum(pc);
+    mp = pc > mp ? pc : mp;
     if (ln == 0) {
       wc[u] = s;
       part[u] = kUnassigned;
     }
   }
+  if (ln == 0 && mp) atomicMax(max_pieces, mp);
 }
 
 // ---------------------------------------------------------------- classify
@@ -97,71 +125,88 @@ __global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const u
 // wl = Σ_{v∈N_u} ld[v] (wedges its traversal reads) and route it to a tier by
 // the partner bound pb = wl - d_u.  Vertices that cannot decrement anybody
 // (d_u < 2, pb == 0, or — peeling — exact support 0) are not traversed; in
-// COUNT mode their support is written as 0 here.  Optionally marks every
-// v ∈ N_u as touched (epoch tag) for the deletion pass.
+// COUNT mode their support is written as 0 here.  Optionally tags every
+// v ∈ N_u with the iteration's epoch (plain store; k_collect_touched lists
+// them for the deletion pass).  One lane per u for d_u <= kSmallDeg; the whole warp for larger degrees.
+constexpr uint32_t kSmallDeg = 64;
 template <int MODE>
 __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
                            const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                            const uint32_t* __restrict__ ld, const uint32_t* __restrict__ part,
                            uint64_t* __restrict__ support, uint2* tier0, uint2* tier1, uint2* tier2,
-                           uint32_t* vflag, uint32_t epoch, uint32_t* touched, Counters* c) {
+                           uint32_t* vflag, uint32_t epoch, Counters* c) {
   const uint32_t ln = lane_id();
   const uint32_t n = list ? *count : nU;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long wsum = 0;
+  unsigned long long wsum = 0, ssum = 0, tw[2] = {0, 0};
   for (uint64_t b = gw * 32; b < n; b += nw * 32) {
-    uint32_t my_u = 0;
-    uint64_t my_wl = 0;
-    bool my_ok = false;
-    const uint32_t cnt = (uint32_t)(n - b < 32 ? n - b : 32);
-    for (uint32_t k = 0; k < cnt; k++) {
-      const uint32_t u = list ? list[b + k] : (uint32_t)(b + k);
-      if (!list && part[u] != kUnassigned) continue;  // warp-uniform
-      uint64_t s = 0;
-      const uint64_t e0 = offU[u], e1 = offU[u + 1];
-      for (uint64_t eb = e0; eb < e1; eb += 32) {  // warp-uniform trip count
+    const uint64_t idx = b + ln;
+    bool ok = idx < n;
+    const uint32_t u = ok ? (list ? list[idx] : (uint32_t)idx) : 0u;
+    if (ok && !list && part[u] != kUnassigned) ok = false;
+    const uint64_t e0 = ok ? offU[u] : 0, d = ok ? offU[u + 1] - e0 : 0;
+    const bool small = d <= kSmallDeg;
+    uint64_t s = 0;
+    // lane-per-vertex pass over small lists
+    uint32_t maxd = small ? (uint32_t)d : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxd = max(maxd, __shfl_xor_sync(kFull, maxd, o));
+    for (uint32_t j = 0; j < maxd; j++) {
+      if (small && j < d) {
+        const uint32_t v = adjU[e0 + j];
+        s += ld[v];
+        if (vflag && vflag[v] != epoch) vflag[v] = epoch;
+      }
+    }
+    // warp-cooperative pass over large lists
+    uint32_t big = __ballot_sync(kFull, ok && !small);
+    while (big) {
+      const int k = __ffs(big) - 1;
+      big &= big - 1;
+      const uint64_t ke0 = __shfl_sync(kFull, e0, k), ke1 = ke0 + __shfl_sync(kFull, d, k);
+      uint64_t ks = 0;
+      for (uint64_t eb = ke0; eb < ke1; eb += 32) {
         const uint64_t e = eb + ln;
-        bool fresh = false;
-        uint32_t v = 0;
-        if (e < e1) {
-          v = adjU[e];
-          s += ld[v];
-          if (vflag && vflag[v] != epoch) fresh = atomicExch(&vflag[v], epoch) != epoch;
+        if (e < ke1) {
+          const uint32_t v = adjU[e];
+          ks += ld[v];
+          if (vflag && vflag[v] != epoch) vflag[v] = epoch;
         }
-        if (vflag) warp_append(fresh, v, touched, &c->ntouched);
       }
-      s = warp_sum(s);
-      if (ln == k) {
-        my_u = u;
-        my_wl = s;
-        my_ok = true;
-      }
+      ks = warp_sum(ks);
+      if ((int)ln == k) s = ks;
     }
     int tier = -1;
     uint32_t pb = 0;
-    if (my_ok) {
-      const uint64_t d = offU[my_u + 1] - offU[my_u];
-      const uint64_t pb64 = my_wl - d;
+    if (ok) {
+      const uint64_t pb64 = s - d;  // u itself appears once in each of its lists
       bool work = d >= 2 && pb64 > 0;
-      if (MODE == 1 && work) work = support[my_u] != 0;
+      if (MODE == 1 && work) work = support[u] != 0;
       if (work) {
         pb = pb64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb64;
-        tier = pb <= kWarpCap ? 0 : (pb <= kCtaCap ? 1 : 2);
-        wsum += my_wl;
+        tier = pb <= kWarpCap ? 0 : 1;
+        wsum += s;
+        ssum += d;
+        tw[tier] += s;
       } else if (MODE == 0) {
-        support[my_u] = 0;
+        support[u] = 0;
       }
     }
-    const uint2 item = make_uint2(my_u, pb);
+    const uint2 item = make_uint2(u, pb);
     warp_append2(tier == 0, item, tier0, &c->ntier[0]);
     warp_append2(tier == 1, item, tier1, &c->ntier[1]);
-    warp_append2(tier == 2, item, tier2, &c->ntier[2]);
   }
   wsum = warp_sum(wsum);
+  ssum = warp_sum(ssum);
+  tw[0] = warp_sum(tw[0]);
+  tw[1] = warp_sum(tw[1]);
   if (ln == 0 && wsum) {
     atomicAdd(&c->wedges, wsum);
     atomicAdd(&c->cum_wedges, wsum);
+    atomicAdd(&c->cum_steps, ssum);
+    if (tw[0]) atomicAdd(&c->tier_wedges[0], tw[0]);
+    if (tw[1]) atomicAdd(&c->tier_wedges[1], tw[1]);
   }
 }
 
@@ -181,10 +226,14 @@ struct AggArgs {
   uint64_t* support;
   const uint2* __restrict__ list;
   const uint32_t* __restrict__ count;
-  uint32_t* slot_cnt;    // heavy tier: per slot dense counters [nU]
-  uint32_t* slot_touch;  // heavy tier: per slot first-touch list [nU]
-  uint32_t* slot_dup;    // heavy tier: per slot w>=2 list [nU]
   uint32_t nU;
+  uint32_t* ticket;      // dynamic scheduling counter (tier 1)
+  uint64_t* piece_pos;   // tier 1 per-CTA piece cursors (piece_cap per CTA)
+  uint64_t* piece_end;
+  uint64_t* piece_save;
+  uint32_t* piece_head;
+  uint32_t* piece_srange;
+  uint64_t piece_cap;
   Counters* c;
 };
 
@@ -249,127 +298,7 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kCtaTierThreads) k_agg_cta(AggArgs a) {
-  extern __shared__ uint32_t sm[];
-  uint32_t* keys = sm;
-  uint32_t* vals = sm + kCtaSlots;
-  uint32_t* s_long = vals + kCtaSlots;              // blockDim entries
-  uint32_t* s_misc = s_long + kCtaTierThreads;      // [0] nlong, [1..34] scan
-  __shared__ unsigned long long s_acc;
-  for (uint32_t s = threadIdx.x; s < kCtaSlots; s += blockDim.x) {
-    keys[s] = kEmpty;
-    vals[s] = 0;
-  }
-  __syncthreads();
-  const uint32_t n = *a.count;
-  const CdLists L{a.adjU, a.offV, a.ld};
-  unsigned long long upd = 0;
-  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const uint2 it = a.list[i];
-    const uint32_t u = it.x;
-    uint32_t logT = ceil_log2(2 * it.y);
-    logT = logT < 5 ? 5 : (logT > 14 ? 14 : logT);
-    if (threadIdx.x == 0) s_acc = 0;
-    auto f = [&](bool ok, uint32_t x) {
-      if (ok && x != u) hash_insert(keys, vals, logT, x);
-    };
-    cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjV, s_long, s_misc, f);
-    uint64_t acc = 0;
-    const uint32_t T = 1u << logT;
-    for (uint32_t s = threadIdx.x; s < T; s += blockDim.x) {
-      const uint32_t k = keys[s];
-      if (k != kEmpty) {
-        const uint32_t wv = vals[s];
-        keys[s] = kEmpty;
-        vals[s] = 0;
-        emit<MODE>(a, k, wv, acc, upd);
-      }
-    }
-    if (MODE == 0) {
-      acc = warp_sum(acc);
-      if (lane_id() == 0 && acc) atomicAdd(&s_acc, (unsigned long long)acc);
-      __syncthreads();
-      if (threadIdx.x == 0) a.support[u] = s_acc;
-    }
-    __syncthreads();
-  }
-  if (MODE == 1) {
-    upd = warp_sum(upd);
-    if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
-  }
-}
-
-// Heavy tier: partners exceed the CTA table.  Each CTA owns a slot of dense
-// global counters over U (the paper's private n-element wedge_count array,
-// P:388-390, space term n·T of P:1419-1424); first touches and w>=2 events
-// are appended to per-slot lists so emission and reset cost O(distinct).
-template <int MODE>
-__global__ void __launch_bounds__(kHeavyThreads) k_agg_heavy(AggArgs a) {
-  __shared__ uint32_t s_long[kHeavyThreads];
-  __shared__ uint32_t s_nlong;
-  __shared__ uint32_t s_ntouch, s_ndup;
-  __shared__ unsigned long long s_acc;
-  uint32_t* cnt = a.slot_cnt + (uint64_t)blockIdx.x * a.nU;
-  uint32_t* touch = a.slot_touch + (uint64_t)blockIdx.x * a.nU;
-  uint32_t* dup = a.slot_dup + (uint64_t)blockIdx.x * a.nU;
-  const uint32_t n = *a.count;
-  const CdLists L{a.adjU, a.offV, a.ld};
-  unsigned long long upd = 0;
-  const uint32_t ln = lane_id();
-  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const uint32_t u = a.list[i].x;
-    if (threadIdx.x == 0) {
-      s_ntouch = 0;
-      s_ndup = 0;
-      s_acc = 0;
-    }
-    __syncthreads();
-    auto f = [&](bool ok, uint32_t x) {
-      bool first = false, second = false;
-      if (ok && x != u) {
-        const uint32_t old = atomicAdd(&cnt[x], 1u);
-        first = old == 0;
-        second = old == 1;
-      }
-      uint32_t m = __ballot_sync(kFull, first);
-      if (m) {
-        uint32_t base = 0;
-        const uint32_t leader = __ffs(m) - 1;
-        if (ln == leader) base = atomicAdd(&s_ntouch, (uint32_t)__popc(m));
-        base = __shfl_sync(kFull, base, leader);
-        if (first) touch[base + __popc(m & lanemask_lt())] = x;
-      }
-      m = __ballot_sync(kFull, second);
-      if (m) {
-        uint32_t base = 0;
-        const uint32_t leader = __ffs(m) - 1;
-        if (ln == leader) base = atomicAdd(&s_ndup, (uint32_t)__popc(m));
-        base = __shfl_sync(kFull, base, leader);
-        if (second) dup[base + __popc(m & lanemask_lt())] = x;
-      }
-    };
-    cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjV, s_long, &s_nlong, f);
-    const uint32_t nd = s_ndup, nt = s_ntouch;
-    uint64_t acc = 0;
-    for (uint32_t j = threadIdx.x; j < nd; j += blockDim.x) {
-      const uint32_t k = dup[j];
-      emit<MODE>(a, k, cnt[k], acc, upd);
-    }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < nt; j += blockDim.x) cnt[touch[j]] = 0;
-    if (MODE == 0) {
-      acc = warp_sum(acc);
-      if (ln == 0 && acc) atomicAdd(&s_acc, (unsigned long long)acc);
-    }
-    __syncthreads();
-    if (MODE == 0 && threadIdx.x == 0) a.support[u] = s_acc;
-  }
-  if (MODE == 1) {
-    upd = warp_sum(upd);
-    if (ln == 0 && upd) atomicAdd(&a.c->updates, upd);
-  }
-}
+#include "agg_range.cuh"
 
 // ---------------------------------------------------------------- range pass
 // Partition start (Alg.4 l.5-8): snapshot ⋈^init = support for all
@@ -447,6 +376,26 @@ __global__ void __launch_bounds__(256) k_select(uint32_t nU, uint32_t* __restric
 }
 
 // ---------------------------------------------------------------- deletion
+// touched = { v : vflag[v] == epoch } (ballots + block scan, one atomic per tile)
+__global__ void __launch_bounds__(256) k_collect_touched(uint32_t nV, const uint32_t* __restrict__ vflag,
+                                                         uint32_t epoch, uint32_t* __restrict__ touched,
+                                                         Counters* c) {
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_base;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < nV; b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = b + threadIdx.x;
+    const bool t = v < nV && vflag[v] == epoch;
+    uint32_t total;
+    const uint32_t r = block_excl_scan(t ? 1u : 0u, s_scan, &total);
+    if (total) {
+      if (threadIdx.x == 0) s_base = atomicAdd(&c->ntouched, total);
+      __syncthreads();
+      if (t) touched[s_base + r] = (uint32_t)v;
+      __syncthreads();
+    }
+  }
+}
+
 // Dynamic graph update: for every touched v, stable-partition
 // the live prefix of N_v into [still live | newly peeled]; the peeled block is
 // placed directly after the live prefix, so over the whole CD each N_v ends as

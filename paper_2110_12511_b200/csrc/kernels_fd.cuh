@@ -120,9 +120,14 @@ struct FdArgs {
   uint32_t* rounds_max;
 };
 
-__device__ __forceinline__ void fd_emit(const FdArgs& a, uint32_t k, uint32_t w, unsigned long long& upd) {
+// s[k] -= C(w,2) for a live partition member; the new value also lowers the
+// next round's level candidate (min over live supports).
+__device__ __forceinline__ void fd_emit(const FdArgs& a, uint32_t k, uint32_t w, unsigned long long& upd,
+                                        unsigned long long* s_min) {
   if (w >= 2 && !a.peeled[k]) {
-    red_add_u64(&a.s[k], 0ull - choose2(w));
+    const uint64_t d = choose2(w);
+    const uint64_t old = atomicAdd((unsigned long long*)&a.s[k], (unsigned long long)(0ull - d));
+    atomicMin(s_min, (unsigned long long)(old - d));
     upd++;
   }
 }
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   uint32_t* htouch = a.slot_touch + (uint64_t)blockIdx.x * a.nU;
   uint32_t* hdup = a.slot_dup + (uint64_t)blockIdx.x * a.nU;
   const FdLists L{a.adjU, a.offV, a.seg};
-  unsigned long long wedges = 0, upd = 0;
+  unsigned long long wedges = 0, upd = 0, steps = 0;
   uint32_t rounds_max = 0;
   __syncthreads();
   for (;;) {
@@ -161,10 +166,10 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
     uint32_t live = a.poff[p + 1] - lo;
     uint64_t k = 0;
     uint32_t rounds = 0;
-    while (live > 0) {
-      // (1) level k = max(k, min live support)
-      if (threadIdx.x == 0) s_min = ~0ull;
-      __syncthreads();
+    // initial level candidate: min support over the partition
+    if (threadIdx.x == 0) s_min = ~0ull;
+    __syncthreads();
+    {
       uint64_t mn = ~0ull;
       for (uint32_t j = threadIdx.x; j < live; j += blockDim.x) {
         const uint64_t v = a.s[a.members[lo + j]];
@@ -172,16 +177,27 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       }
       mn = warp_min_u64(mn);
       if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
-      __syncthreads();
+    }
+    __syncthreads();
+    while (live > 0) {
+      // (1) level k = max(k, min live support); s_min was maintained by the
+      //     previous round's selection scan and its decrements
       k = s_min > k ? s_min : k;
-      // (2) select {support <= k}: θ = k; compact the rest in place
+      __syncthreads();
+      if (threadIdx.x == 0) s_min = ~0ull;
+      __syncthreads();
+      // (2) select {support <= k}: θ = k; compact the rest in place and
+      //     start the next level candidate from the kept supports
       uint32_t nsel = 0, nkeep = 0;
+      uint64_t mn = ~0ull;
       for (uint32_t c0 = 0; c0 < live; c0 += blockDim.x) {
         const uint32_t j = c0 + threadIdx.x;
         const bool ok = j < live;
         const uint32_t u = ok ? a.members[lo + j] : 0u;
-        const bool sl = ok && a.s[u] <= k;
+        const uint64_t su = ok ? a.s[u] : ~0ull;
+        const bool sl = ok && su <= k;
         const bool kp = ok && !sl;
+        if (kp) mn = su < mn ? su : mn;
         uint32_t ts, tk;
         const uint32_t rs = block_excl_scan(sl ? 1u : 0u, s_scan, &ts);
         const uint32_t rk = block_excl_scan(kp ? 1u : 0u, s_scan, &tk);
@@ -196,6 +212,8 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       }
       live = nkeep;
       rounds++;
+      mn = warp_min_u64(mn);
+      if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
       __syncthreads();
       // (3) partner bound of each selected vertex inside G_p
       for (uint32_t j = w; j < nsel; j += nw) {
@@ -216,6 +234,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
           if (d >= 2 && pb > 0 && a.s[u] != 0) {
             r = pb > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb;
             wedges += wl;
+            steps += d;
           }
           a.selpb[lo + j] = r;
         }
@@ -239,7 +258,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
             const uint32_t wv = wvals[s];
             wkeys[s] = kEmpty;
             wvals[s] = 0;
-            fd_emit(a, key, wv, upd);
+            fd_emit(a, key, wv, upd, &s_min);
           }
         }
         __syncwarp();
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
               const uint32_t wv = cvals[s];
               ckeys[s] = kEmpty;
               cvals[s] = 0;
-              fd_emit(a, key, wv, upd);
+              fd_emit(a, key, wv, upd, &s_min);
             }
           }
           __syncthreads();
@@ -301,7 +320,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
           const uint32_t nd = s_ndup, nt = s_ntouch;
           for (uint32_t q = threadIdx.x; q < nd; q += blockDim.x) {
             const uint32_t key = hdup[q];
-            fd_emit(a, key, hcnt[key], upd);
+            fd_emit(a, key, hcnt[key], upd, &s_min);
           }
           __syncthreads();
           for (uint32_t q = threadIdx.x; q < nt; q += blockDim.x) hcnt[htouch[q]] = 0;
@@ -314,9 +333,11 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   }
   wedges = warp_sum(wedges);
   upd = warp_sum(upd);
+  steps = warp_sum(steps);
   if (ln == 0) {
     if (wedges) atomicAdd(a.wedges, wedges);
     if (upd) atomicAdd(a.updates, upd);
+    if (steps) atomicAdd(a.wedges + 2, steps);
   }
   if (threadIdx.x == 0) atomicMax(a.rounds_max, rounds_max);
 }

@@ -39,12 +39,11 @@ void check(cudaError_t e, const char* what, int line) {
   }
 }
 #define CK(x) check((x), #x, __LINE__)
-#define LAUNCHED(name) check(cudaGetLastError(), "launch " name, __LINE__)
 
 constexpr uint64_t kInf = ~0ull;
 
 size_t warp_tier_smem() { return (size_t)(kWarpTierThreads / 32) * 2 * kWarpSlots * 4; }
-size_t cta_tier_smem() { return ((size_t)2 * kCtaSlots + kCtaTierThreads + 40) * 4; }
+size_t range_smem() { return sizeof(RangeSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
 size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kCtaSlots + kFdThreads) * 4; }
 
@@ -53,8 +52,8 @@ void set_attrs_once() {
   std::call_once(once, [] {
     cudaFuncSetAttribute(k_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
-    cudaFuncSetAttribute(k_agg_cta<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_tier_smem());
-    cudaFuncSetAttribute(k_agg_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_tier_smem());
+    cudaFuncSetAttribute(k_agg_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
+    cudaFuncSetAttribute(k_agg_range<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
     cudaFuncSetAttribute(k_range_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem());
     cudaFuncSetAttribute(k_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem());
     cudaGetLastError();
@@ -106,6 +105,31 @@ class Run {
     CK(cudaEventRecord(e, st));
     return e;
   }
+  // kernel launch bookkeeping: launch count always; per-family device time
+  // (CUDA events on the launch stream) when `timing` is set (PBNG_OPT_STATS)
+  void pre(int kind) {
+    (void)kind;
+    pending = nullptr;
+    if (timing) {
+      CK(cudaEventCreate(&pending));
+      CK(cudaEventRecord(pending, st));
+    }
+  }
+  void post(int kind) {
+    check(cudaGetLastError(), "kernel launch", kind);
+    launches++;
+    if (timing) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, st));
+      spans.push_back({kind, pending, e});
+      events.push_back(pending);
+      events.push_back(e);
+    }
+  }
+  void kernel_ms(float* out) {
+    for (const Span& sp : spans) out[sp.kind] += elapsed_(sp.a, sp.b);
+  }
   Counters& readback(Counters* dc) {
     CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -114,8 +138,21 @@ class Run {
   cudaStream_t st;
   int nsm = 148;
   Counters* hc = nullptr;
+  bool timing = false;
+  uint32_t launches = 0;
 
  private:
+  struct Span {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  static float elapsed_(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  cudaEvent_t pending = nullptr;
+  std::vector<Span> spans;
   std::vector<void*> allocs;
   std::vector<cudaEvent_t> events;
 };
@@ -129,9 +166,12 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 void validate(Run& r, const Dev& g) {
   uint32_t* bad = r.alloc<uint32_t>(1);
   CK(cudaMemsetAsync(bad, 0, 4, r.st));
+  r.pre(PBNG_K_INIT);
   k_validate_csr<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, g.m, g.offU, g.adjU, g.nV, bad);
+  r.post(PBNG_K_INIT);
+  r.pre(PBNG_K_INIT);
   k_validate_csr<<<r.nsm * 4, 256, 0, r.st>>>(g.nV, g.m, g.offV, g.adjV, g.nU, bad);
-  LAUNCHED("k_validate_csr");
+  r.post(PBNG_K_INIT);
   uint32_t hb = 0;
   CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, r.st));
   CK(cudaStreamSynchronize(r.st));
@@ -157,7 +197,11 @@ struct State {
   uint32_t* hist_n;
   unsigned long long* sum_d2;
   uint32_t nslots;
-  uint32_t *slot_cnt, *slot_touch, *slot_dup;
+  uint32_t *slot_cnt, *slot_touch, *slot_dup;  // FD heavy path: dense counters per CTA
+  uint64_t piece_cap;                          // tier-1 cursor scratch per CTA
+  uint64_t *piece_pos, *piece_end, *piece_save;
+  uint32_t* piece_head;
+  uint32_t* piece_srange;
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -187,19 +231,28 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live) {
   S.hist_w = r.alloc<unsigned long long>(kBins);
   S.hist_n = r.alloc<uint32_t>(kBins);
   S.sum_d2 = r.alloc<unsigned long long>(1);
-  S.nslots = choose_slots(r, g.nU);
-  S.slot_cnt = r.alloc<uint32_t>((size_t)S.nslots * g.nU);
-  S.slot_touch = r.alloc<uint32_t>((size_t)S.nslots * g.nU);
-  S.slot_dup = r.alloc<uint32_t>((size_t)S.nslots * g.nU);
-  CK(cudaMemsetAsync(S.slot_cnt, 0, (size_t)S.nslots * g.nU * 4, r.st));
   CK(cudaMemsetAsync(S.vflag, 0, (size_t)std::max<uint32_t>(g.nV, 1) * 4, r.st));
   CK(cudaMemsetAsync(S.c, 0, sizeof(Counters), r.st));
   CK(cudaMemsetAsync(S.sum_d2, 0, 8, r.st));
   if (need_live && g.m) CK(cudaMemcpyAsync(S.adjL, g.adjV, g.m * 4, cudaMemcpyDeviceToDevice, r.st));
+  r.pre(PBNG_K_INIT);
   k_init_v<<<r.nsm * 4, 256, 0, r.st>>>(g.nV, g.offV, S.ld, S.sum_d2);
-  LAUNCHED("k_init_v");
-  k_init_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, g.offV, S.wc, S.part);
-  LAUNCHED("k_init_u");
+  r.post(PBNG_K_INIT);
+  unsigned long long* dmax = r.alloc<unsigned long long>(1);
+  CK(cudaMemsetAsync(dmax, 0, 8, r.st));
+  r.pre(PBNG_K_INIT);
+  k_init_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, g.offV, S.wc, S.part, dmax);
+  r.post(PBNG_K_INIT);
+  unsigned long long hmax = 0;
+  CK(cudaMemcpyAsync(&hmax, dmax, 8, cudaMemcpyDeviceToHost, r.st));
+  CK(cudaStreamSynchronize(r.st));
+  S.piece_cap = std::max<unsigned long long>(hmax, 1);
+  const size_t np = (size_t)r.nsm * kRangeCtas * S.piece_cap;
+  S.piece_pos = r.alloc<uint64_t>(np);
+  S.piece_end = r.alloc<uint64_t>(np);
+  S.piece_save = r.alloc<uint64_t>(np);
+  S.piece_head = r.alloc<uint32_t>(np);
+  S.piece_srange = r.alloc<uint32_t>(np);
 }
 
 AggArgs agg_args(const State& S, int t) {
@@ -213,46 +266,56 @@ AggArgs agg_args(const State& S, int t) {
   a.support = S.support;
   a.list = S.tier[t];
   a.count = &S.c->ntier[t];
-  a.slot_cnt = S.slot_cnt;
-  a.slot_touch = S.slot_touch;
-  a.slot_dup = S.slot_dup;
   a.nU = S.g.nU;
+  a.ticket = &S.c->ticket[t];
+  a.piece_pos = S.piece_pos;
+  a.piece_end = S.piece_end;
+  a.piece_save = S.piece_save;
+  a.piece_head = S.piece_head;
+  a.piece_srange = S.piece_srange;
+  a.piece_cap = S.piece_cap;
   a.c = S.c;
   return a;
 }
 
 template <int MODE>
 void launch_agg(Run& r, const State& S) {
+  r.pre(PBNG_K_AGG_WARP);
   k_agg_warp<MODE><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
-  LAUNCHED("k_agg_warp");
-  k_agg_cta<MODE><<<r.nsm, kCtaTierThreads, cta_tier_smem(), r.st>>>(agg_args(S, 1));
-  LAUNCHED("k_agg_cta");
-  k_agg_heavy<MODE><<<S.nslots, kHeavyThreads, 0, r.st>>>(agg_args(S, 2));
-  LAUNCHED("k_agg_heavy");
+  r.post(PBNG_K_AGG_WARP);
+  r.pre(PBNG_K_AGG_CTA);
+  k_agg_range<MODE><<<r.nsm * kRangeCtas, kRangeThreads, range_smem(), r.st>>>(agg_args(S, 1));
+  r.post(PBNG_K_AGG_CTA);
 }
 
 void reset_tiers(Run& r, State& S) {
-  CK(cudaMemsetAsync(&S.c->ntier[0], 0, 3 * sizeof(uint32_t), r.st));
+  CK(cudaMemsetAsync(&S.c->ntier[0], 0, 7 * sizeof(uint32_t), r.st));  // ntier[3] + ticket[4]
 }
 
 // Butterfly count of every unassigned u (initial count, and §5.1 re-count).
 void count_live(Run& r, State& S) {
   reset_tiers(r, S);
+  r.pre(PBNG_K_CLASSIFY);
   k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(S.g.nU, nullptr, nullptr, S.g.offU, S.g.adjU, S.ld, S.part,
-                                               S.support, S.tier[0], S.tier[1], S.tier[2], nullptr, 0, nullptr,
-                                               S.c);
-  LAUNCHED("k_classify<count>");
+                                               S.support, S.tier[0], S.tier[1], S.tier[2], nullptr, 0, S.c);
+  r.post(PBNG_K_CLASSIFY);
   launch_agg<0>(r, S);
 }
 
-void compact(Run& r, State& S) {
+void compact(Run& r, State& S, uint32_t epoch) {
   const uint32_t big = 4096;
+  CK(cudaMemsetAsync(&S.c->ntouched, 0, 4, r.st));
+  r.pre(PBNG_K_COMPACT);
+  k_collect_touched<<<r.nsm * 8, 256, 0, r.st>>>(S.g.nV, S.vflag, epoch, S.touched, S.c);
+  r.post(PBNG_K_COMPACT);
+  r.pre(PBNG_K_COMPACT);
   k_compact<<<r.nsm * 8, 256, 0, r.st>>>(S.touched, &S.c->ntouched, S.g.offV, S.adjL, S.tmp, S.ld, S.part, big,
                                          S.c);
-  LAUNCHED("k_compact");
+  r.post(PBNG_K_COMPACT);
+  r.pre(PBNG_K_COMPACT);
   k_compact_big<<<r.nsm, 512, 0, r.st>>>(S.touched, &S.c->ntouched, S.g.offV, S.adjL, S.tmp, S.ld, S.part, big,
                                          S.c);
-  LAUNCHED("k_compact_big");
+  r.post(PBNG_K_COMPACT);
 }
 
 struct Plan {
@@ -276,9 +339,10 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
     CK(cudaMemsetAsync(S.hist_w, 0, kBins * 8, r.st));
     CK(cudaMemsetAsync(S.hist_n, 0, kBins * 4, r.st));
     CK(cudaMemsetAsync(&S.c->live_wc, 0, 16, r.st));
+    r.pre(PBNG_K_RANGE);
     k_range_hist<<<r.nsm, 1024, hist_smem(), r.st>>>(nU, S.part, S.support, S.wc, S.init, S.hist_w, S.hist_n,
                                                      S.c);
-    LAUNCHED("k_range_hist");
+    r.post(PBNG_K_RANGE);
     CK(cudaMemcpyAsync(hw.data(), S.hist_w, kBins * 8, cudaMemcpyDeviceToHost, r.st));
     CK(cudaMemcpyAsync(hn.data(), S.hist_n, kBins * 4, cudaMemcpyDeviceToHost, r.st));
     const Counters hc0 = r.readback(S.c);
@@ -313,12 +377,13 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         epoch++;
         CK(cudaMemsetAsync(&S.c->ntouched, 0, 4, r.st));
       }
+      r.pre(PBNG_K_SELECT);
       k_select<<<r.nsm * 8, 256, 0, r.st>>>(nU, S.part, S.support, S.wc, bound, pid, S.F, S.c);
-      LAUNCHED("k_select");
+      r.post(PBNG_K_SELECT);
+      r.pre(PBNG_K_CLASSIFY);
       k_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(nU, S.F, &S.c->nF, S.g.offU, S.g.adjU, S.ld, S.part, S.support,
-                                                   S.tier[0], S.tier[1], S.tier[2], S.vflag, epoch, S.touched,
-                                                   S.c);
-      LAUNCHED("k_classify<peel>");
+                                                   S.tier[0], S.tier[1], S.tier[2], S.vflag, epoch, S.c);
+      r.post(PBNG_K_CLASSIFY);
       const Counters hc = r.readback(S.c);
       if (hc.nF == 0) break;
       st.rho_cd_iters++;
@@ -327,7 +392,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
       part_wc += hc.sel_wc;
       if (bound == kInf) {
         // every live vertex is in this batch: nobody is left to update
-        if (del) compact(r, S);
+        if (del) compact(r, S, epoch);
         continue;
       }
       const unsigned long long recount_cost = sum_d2 - hc.ld2_drop;  // one-sided re-count cost (g10)
@@ -335,15 +400,15 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
                            ((opts & PBNG_OPT_FORCE_RECOUNT) || hc.wedges > recount_cost);
       if (recount) {
         // §5.1: re-compute supports of all remaining vertices
-        if (del) compact(r, S);
+        if (del) compact(r, S, epoch);
         count_live(r, S);
         st.recounts++;
       } else {
         launch_agg<1>(r, S);
-        if (del) compact(r, S);
+        if (del) compact(r, S, epoch);
       }
     }
-    if (!del) compact(r, S);
+    if (!del) compact(r, S, epoch);
     scale = part_wc ? (double)first_wc / (double)part_wc : 1.0;
   }
   plan.nparts = (uint32_t)plan.bounds.size() - 1;
@@ -354,6 +419,11 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
 void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st, float& ms_build) {
   const uint32_t np = plan.nparts, nU = S.g.nU;
   cudaEvent_t e0 = r.event();
+  S.nslots = choose_slots(r, nU);
+  S.slot_cnt = r.alloc<uint32_t>((size_t)S.nslots * nU);
+  S.slot_touch = r.alloc<uint32_t>((size_t)S.nslots * nU);
+  S.slot_dup = r.alloc<uint32_t>((size_t)S.nslots * nU);
+  CK(cudaMemsetAsync(S.slot_cnt, 0, (size_t)S.nslots * nU * 4, r.st));
   uint32_t* pcount = r.alloc<uint32_t>(np);
   uint32_t* poff = r.alloc<uint32_t>(np + 1);
   uint32_t* pcur = r.alloc<uint32_t>(np);
@@ -372,18 +442,21 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   CK(cudaMemsetAsync(peeled, 0, nU, r.st));
   CK(cudaMemsetAsync(fdc, 0, 24, r.st));
   CK(cudaMemsetAsync(misc, 0, 8, r.st));
+  r.pre(PBNG_K_FD_BUILD);
   k_part_count<<<r.nsm * 4, 256, np * 4, r.st>>>(nU, S.part, np, pcount);
-  LAUNCHED("k_part_count");
+  r.post(PBNG_K_FD_BUILD);
   std::vector<uint32_t> hcount(np), hoff(np + 1);
   CK(cudaMemcpyAsync(hcount.data(), pcount, (size_t)np * 4, cudaMemcpyDeviceToHost, r.st));
   CK(cudaStreamSynchronize(r.st));
   hoff[0] = 0;
   for (uint32_t i = 0; i < np; i++) hoff[i + 1] = hoff[i] + hcount[i];
   CK(cudaMemcpyAsync(poff, hoff.data(), (size_t)(np + 1) * 4, cudaMemcpyHostToDevice, r.st));
+  r.pre(PBNG_K_FD_BUILD);
   k_part_scatter<<<r.nsm * 8, 256, 0, r.st>>>(nU, S.part, poff, pcur, members);
-  LAUNCHED("k_part_scatter");
+  r.post(PBNG_K_FD_BUILD);
+  r.pre(PBNG_K_FD_BUILD);
   k_fd_seg<<<r.nsm * 8, 256, np * 8, r.st>>>(nU, S.g.offU, S.g.adjU, S.g.offV, S.adjL, S.part, np, seg, work);
-  LAUNCHED("k_fd_seg");
+  r.post(PBNG_K_FD_BUILD);
   std::vector<unsigned long long> hwork(np);
   CK(cudaMemcpyAsync(hwork.data(), work, (size_t)np * 8, cudaMemcpyDeviceToHost, r.st));
   CK(cudaStreamSynchronize(r.st));
@@ -418,8 +491,9 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   a.updates = fdc + 1;
   a.rounds_max = misc + 1;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>({np, (uint32_t)r.nsm, S.nslots}));
+  r.pre(PBNG_K_FD);
   k_fd<<<grid, kFdThreads, fd_smem(), r.st>>>(a);
-  LAUNCHED("k_fd");
+  r.post(PBNG_K_FD);
   cudaEvent_t e2 = r.event();
   unsigned long long hf[3];
   uint32_t hm[2];
@@ -428,6 +502,9 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   CK(cudaStreamSynchronize(r.st));
   st.wedges_fd = hf[0];
   st.support_updates += hf[1];
+  st.uv_steps += hf[2];
+  st.uv_steps_fd = hf[2];
+  st.updates_fd = hf[1];
   st.fd_rounds_max = hm[1];
   ms_build = elapsed(e0, e1);
   st.ms_fd = elapsed(e1, e2);
@@ -463,6 +540,7 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   pbng_stats st;
   std::memset(&st, 0, sizeof(st));
   Run r(s);
+  r.timing = (opts & PBNG_OPT_STATS) != 0;
   if (opts & PBNG_OPT_VALIDATE) validate(r, g);
   if (g.nU == 0) {
     if (out.bounds) {
@@ -487,6 +565,8 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   const Counters c1 = r.readback(S.c);
   st.support_updates += c1.updates;
   st.wedges_cd = c1.cum_wedges - c0.cum_wedges;
+  for (int i = 0; i < 4; i++) st.impl[i] = c1.dbg[i];
+  st.uv_steps += c1.cum_steps;
   st.ms_count = elapsed(t0, t1);
   st.ms_cd = elapsed(t1, t2);
   if (out.part) {
@@ -501,6 +581,9 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
     run_fd(r, S, plan, out.tip, st, ms_build);
     st.ms_fd_build = ms_build;
   }
+  CK(cudaStreamSynchronize(r.st));
+  st.launches = r.launches;
+  if (r.timing) r.kernel_ms(st.ms_kernel);
   if (stats) *stats = st;
 }
 

@@ -48,5 +48,5 @@ def test_missing_library_fails_loudly(tmp_path):
 
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(pbng.Csr) == 32
-    assert ctypes.sizeof(pbng.Stats) == 4 * 8 + 4 * 4 + 4 * 4
+    assert ctypes.sizeof(pbng.Stats) == 4 * 8 + 4 * 4 + 4 * 4 + 3 * 8 + 8 + 4 * 8 + 16 * 4
     assert pbng.MAX_P == 4096
