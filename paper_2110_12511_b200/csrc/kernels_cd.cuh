@@ -127,15 +127,19 @@ __global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const u
 // (d_u < 2, pb == 0, or — peeling — exact support 0) are not traversed; in
 // COUNT mode their support is written as 0 here.  Optionally tags every
 // v ∈ N_u with the iteration's epoch (plain store; k_collect_touched lists
-// them for the deletion pass).  One lane per u for d_u <= kSmallDeg; the whole warp for larger degrees.
-constexpr uint32_t kSmallDeg = 64;
+// them for the deletion pass).
+// A warp takes 32 vertices and walks their edges as one flattened range
+// (binary search over the lanes' inclusive degree scan), so every lane issues
+// independent loads regardless of the degree mix.
 template <int MODE>
 __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
                            const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                            const uint32_t* __restrict__ ld, const uint32_t* __restrict__ part,
                            uint64_t* __restrict__ support, uint2* tier0, uint2* tier1, uint2* tier2,
                            uint32_t* vflag, uint32_t epoch, Counters* c) {
-  const uint32_t ln = lane_id();
+  __shared__ unsigned long long s_acc[8][32];  // launched with 256 threads
+  const uint32_t ln = lane_id(), wib = threadIdx.x >> 5;
+  unsigned long long* acc = s_acc[wib & 7];
   const uint32_t n = list ? *count : nU;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -146,37 +150,46 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
     const uint32_t u = ok ? (list ? list[idx] : (uint32_t)idx) : 0u;
     if (ok && !list && part[u] != kUnassigned) ok = false;
     const uint64_t e0 = ok ? offU[u] : 0, d = ok ? offU[u + 1] - e0 : 0;
-    const bool small = d <= kSmallDeg;
-    uint64_t s = 0;
-    // lane-per-vertex pass over small lists
-    uint32_t maxd = small ? (uint32_t)d : 0u;
+    acc[ln] = 0;
+    // inclusive scan of degrees over the warp (64-bit: a warp may hold hubs)
+    uint64_t incl = d;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) maxd = max(maxd, __shfl_xor_sync(kFull, maxd, o));
-    for (uint32_t j = 0; j < maxd; j++) {
-      if (small && j < d) {
-        const uint32_t v = adjU[e0 + j];
-        s += ld[v];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, incl, o);
+      if (ln >= (uint32_t)o) incl += y;
+    }
+    const uint64_t total = __shfl_sync(kFull, incl, 31);
+    const uint64_t excl = incl - d;
+    __syncwarp();
+    for (uint64_t t0 = 0; t0 < total; t0 += 32) {
+      const uint64_t t = t0 + ln;
+      uint32_t j = 0;
+#pragma unroll
+      for (uint32_t s2 = 16; s2 > 0; s2 >>= 1) {
+        const uint64_t y = __shfl_sync(kFull, incl, j + s2 - 1);
+        if (y <= t) j += s2;
+      }
+      const uint64_t je = __shfl_sync(kFull, e0, j), jx = __shfl_sync(kFull, excl, j);
+      const bool valid = t < total;
+      unsigned long long val = 0;
+      if (valid) {
+        const uint32_t v = adjU[je + (t - jx)];
+        val = ld[v];
         if (vflag && vflag[v] != epoch) vflag[v] = epoch;
       }
-    }
-    // warp-cooperative pass over large lists
-    uint32_t big = __ballot_sync(kFull, ok && !small);
-    while (big) {
-      const int k = __ffs(big) - 1;
-      big &= big - 1;
-      const uint64_t ke0 = __shfl_sync(kFull, e0, k), ke1 = ke0 + __shfl_sync(kFull, d, k);
-      uint64_t ks = 0;
-      for (uint64_t eb = ke0; eb < ke1; eb += 32) {
-        const uint64_t e = eb + ln;
-        if (e < ke1) {
-          const uint32_t v = adjU[e];
-          ks += ld[v];
-          if (vflag && vflag[v] != epoch) vflag[v] = epoch;
-        }
+      // segmented sum over lanes with the same vertex j (contiguous in lane order)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, val, o);
+        const uint32_t yj = __shfl_up_sync(kFull, j, o);
+        if (ln >= (uint32_t)o && yj == j) val += y;
       }
-      ks = warp_sum(ks);
-      if ((int)ln == k) s = ks;
+      const uint32_t nj = __shfl_down_sync(kFull, j, 1);
+      if (valid && (ln == 31 || nj != j || t + 1 >= total)) acc[j] += val;
+      __syncwarp();
     }
+    __syncwarp();
+    const uint64_t s = acc[ln];
     int tier = -1;
     uint32_t pb = 0;
     if (ok) {
@@ -196,6 +209,7 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
     const uint2 item = make_uint2(u, pb);
     warp_append2(tier == 0, item, tier0, &c->ntier[0]);
     warp_append2(tier == 1, item, tier1, &c->ntier[1]);
+    __syncwarp();
   }
   wsum = warp_sum(wsum);
   ssum = warp_sum(ssum);

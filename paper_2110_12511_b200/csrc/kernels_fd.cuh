@@ -64,10 +64,12 @@ __device__ __forceinline__ uint32_t desc_bound(const uint32_t* __restrict__ list
 // For every U-edge (u, v): the segment N_v ∩ U_part[u] of the partition-ordered
 // list (seg = lo | hi << 32), and the LPT work estimate
 // work[p] = Σ_{u∈U_p} Σ_{v∈N_u} |N_v ∩ U_p| = Σ_v |N_v ∩ U_p|^2  (g13).
+// Also counts the vertices whose FD partner bound exceeds the CTA table
+// (*nheavy), which decides whether FD needs its dense-counter slots.
 __global__ void k_fd_seg(uint32_t nU, const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                          const uint64_t* __restrict__ offV, const uint32_t* __restrict__ adjL,
                          const uint32_t* __restrict__ part, uint32_t nparts, uint64_t* __restrict__ seg,
-                         unsigned long long* work) {
+                         unsigned long long* work, uint32_t* nheavy) {
   extern __shared__ unsigned long long sw[];
   for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x) sw[i] = 0;
   __syncthreads();
@@ -87,7 +89,11 @@ __global__ void k_fd_seg(uint32_t nU, const uint64_t* __restrict__ offU, const u
       acc += hi - lo;
     }
     acc = warp_sum(acc);
-    if (ln == 0 && acc) atomicAdd(&sw[p], acc);
+    if (ln == 0 && acc) {
+      atomicAdd(&sw[p], acc);
+      const uint64_t d = offU[u + 1] - offU[u];
+      if (acc - d > kCtaCap) atomicAdd(nheavy, 1u);
+    }
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x)
@@ -106,11 +112,13 @@ struct FdArgs {
   const uint32_t* __restrict__ order;  // partition ids, decreasing work (LPT)
   uint32_t nparts;
   uint32_t* ticket;
-  uint32_t* members;  // live list per partition (compacted in place)
+  uint32_t* members;  // per partition: vertices not yet in the candidate band (compacted at band refills)
+  uint32_t* cand;     // per partition: candidate band C ⊇ {live : support <= T}
   uint32_t* sel;      // vertices peeled this round
   uint32_t* selpb;    // partner bound per selected vertex (0 = nothing to update)
+  uint32_t* bigl;     // indices (into sel) of selected vertices handled by the whole CTA
   uint64_t* s;        // FD supports, initialised to ⋈^init
-  uint8_t* peeled;
+  uint32_t* state;    // 0 = in members, 1 = in cand, 2 = peeled
   uint64_t* theta;
   uint32_t* slot_cnt;
   uint32_t* slot_touch;
@@ -120,15 +128,22 @@ struct FdArgs {
   uint32_t* rounds_max;
 };
 
-// s[k] -= C(w,2) for a live partition member; the new value also lowers the
-// next round's level candidate (min over live supports).
+struct FdBand {        // shared-memory view of the partition being peeled
+  uint32_t lo;         // partition offset into members / cand / sel
+  uint32_t nc;         // candidate count (grows when decrements cross T)
+  unsigned long long T;
+};
+
+// s[k] -= C(w,2) for a live partition member; a member of the rest whose
+// support drops to <= T joins the candidate band.
 __device__ __forceinline__ void fd_emit(const FdArgs& a, uint32_t k, uint32_t w, unsigned long long& upd,
-                                        unsigned long long* s_min) {
-  if (w >= 2 && !a.peeled[k]) {
+                                        FdBand& band) {
+  if (w >= 2 && a.state[k] != 2) {
     const uint64_t d = choose2(w);
     const uint64_t old = atomicAdd((unsigned long long*)&a.s[k], (unsigned long long)(0ull - d));
-    atomicMin(s_min, (unsigned long long)(old - d));
     upd++;
+    if (old - d <= band.T && a.state[k] == 0 && atomicCAS(&a.state[k], 0u, 1u) == 0u)
+      a.cand[band.lo + atomicAdd(&band.nc, 1u)] = k;
   }
 }
 
@@ -141,8 +156,9 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   uint32_t* cvals = ckeys + kCtaSlots;
   uint32_t* s_long = cvals + kCtaSlots;
   __shared__ uint32_t s_scan[33];
-  __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t;
+  __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t, s_nbig;
   __shared__ unsigned long long s_min;
+  __shared__ FdBand band;
   for (uint32_t i = threadIdx.x; i < nw * 2 * kFdWarpSlots; i += blockDim.x) sm[i] = (i / kFdWarpSlots) % 2 == 0 ? kEmpty : 0u;
   for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) {
     ckeys[i] = kEmpty;
@@ -163,57 +179,102 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
     if (t >= a.nparts) break;
     const uint32_t p = a.order[t];
     const uint32_t lo = a.poff[p];
-    uint32_t live = a.poff[p + 1] - lo;
+    uint32_t nrest = a.poff[p + 1] - lo;
     uint64_t k = 0;
     uint32_t rounds = 0;
-    // initial level candidate: min support over the partition
-    if (threadIdx.x == 0) s_min = ~0ull;
-    __syncthreads();
-    {
-      uint64_t mn = ~0ull;
-      for (uint32_t j = threadIdx.x; j < live; j += blockDim.x) {
-        const uint64_t v = a.s[a.members[lo + j]];
-        mn = v < mn ? v : mn;
-      }
-      mn = warp_min_u64(mn);
-      if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
+    if (threadIdx.x == 0) {
+      band.lo = lo;
+      band.nc = 0;
+      band.T = 0;
     }
     __syncthreads();
-    while (live > 0) {
-      // (1) level k = max(k, min live support); s_min was maintained by the
-      //     previous round's selection scan and its decrements
-      k = s_min > k ? s_min : k;
-      __syncthreads();
+    for (;;) {
+      uint32_t nc = band.nc;
+      if (nc == 0) {
+        // (0) candidate band refill: T = m + max(m/8, 8) from the rest's minimum m;
+        //     members with support <= T move to cand, the rest is compacted
+        if (threadIdx.x == 0) s_min = ~0ull;
+        __syncthreads();
+        uint64_t mn = ~0ull;
+        for (uint32_t j = threadIdx.x; j < nrest; j += blockDim.x) {
+          const uint32_t u = a.members[lo + j];
+          if (a.state[u] == 0) {
+            const uint64_t v = a.s[u];
+            mn = v < mn ? v : mn;
+          }
+        }
+        mn = warp_min_u64(mn);
+        if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
+        __syncthreads();
+        const uint64_t m = s_min;
+        if (m == ~0ull) break;  // partition done
+        const uint64_t gap = (m >> 3) > 8 ? (m >> 3) : 8;
+        const uint64_t T = m > ~0ull - gap ? ~0ull : m + gap;
+        uint32_t nkeep = 0;
+        for (uint32_t c0 = 0; c0 < nrest; c0 += blockDim.x) {
+          const uint32_t j = c0 + threadIdx.x;
+          const uint32_t u = j < nrest ? a.members[lo + j] : 0u;
+          const bool lv = j < nrest && a.state[u] == 0;
+          const bool in = lv && a.s[u] <= T;
+          const bool kp = lv && !in;
+          uint32_t ti, tk;
+          const uint32_t ri = block_excl_scan(in ? 1u : 0u, s_scan, &ti);
+          const uint32_t rk = block_excl_scan(kp ? 1u : 0u, s_scan, &tk);
+          if (in) {
+            a.cand[lo + nc + ri] = u;
+            a.state[u] = 1;
+          }
+          if (kp) a.members[lo + nkeep + rk] = u;
+          nc += ti;
+          nkeep += tk;
+        }
+        nrest = nkeep;
+        if (threadIdx.x == 0) {
+          band.nc = nc;
+          band.T = T;
+        }
+        __syncthreads();
+      }
+      // (1) level k = max(k, min support over the band) — every live vertex
+      //     with support <= T is in the band, so this is the live minimum
       if (threadIdx.x == 0) s_min = ~0ull;
       __syncthreads();
-      // (2) select {support <= k}: θ = k; compact the rest in place and
-      //     start the next level candidate from the kept supports
+      {
+        uint64_t mn = ~0ull;
+        for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
+          const uint64_t v = a.s[a.cand[lo + j]];
+          mn = v < mn ? v : mn;
+        }
+        mn = warp_min_u64(mn);
+        if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
+      }
+      __syncthreads();
+      k = s_min > k ? s_min : k;
+      // (2) select {support <= k} from the band: θ = k; compact the band
       uint32_t nsel = 0, nkeep = 0;
-      uint64_t mn = ~0ull;
-      for (uint32_t c0 = 0; c0 < live; c0 += blockDim.x) {
+      for (uint32_t c0 = 0; c0 < nc; c0 += blockDim.x) {
         const uint32_t j = c0 + threadIdx.x;
-        const bool ok = j < live;
-        const uint32_t u = ok ? a.members[lo + j] : 0u;
-        const uint64_t su = ok ? a.s[u] : ~0ull;
-        const bool sl = ok && su <= k;
+        const bool ok = j < nc;
+        const uint32_t u = ok ? a.cand[lo + j] : 0u;
+        const bool sl = ok && a.s[u] <= k;
         const bool kp = ok && !sl;
-        if (kp) mn = su < mn ? su : mn;
         uint32_t ts, tk;
         const uint32_t rs = block_excl_scan(sl ? 1u : 0u, s_scan, &ts);
         const uint32_t rk = block_excl_scan(kp ? 1u : 0u, s_scan, &tk);
         if (sl) {
           a.sel[lo + nsel + rs] = u;
           a.theta[u] = k;
-          a.peeled[u] = 1;
+          a.state[u] = 2;
         }
-        if (kp) a.members[lo + nkeep + rk] = u;
+        if (kp) a.cand[lo + nkeep + rk] = u;
         nsel += ts;
         nkeep += tk;
       }
-      live = nkeep;
       rounds++;
-      mn = warp_min_u64(mn);
-      if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
+      if (threadIdx.x == 0) {
+        band.nc = nkeep;
+        s_nbig = 0;
+      }
       __syncthreads();
       // (3) partner bound of each selected vertex inside G_p
       for (uint32_t j = w; j < nsel; j += nw) {
@@ -237,6 +298,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
             steps += d;
           }
           a.selpb[lo + j] = r;
+          if (r > kFdWarpCap) a.bigl[lo + atomicAdd(&s_nbig, 1u)] = j;  // whole-CTA work, step (5)
         }
       }
       __syncthreads();
@@ -258,16 +320,17 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
             const uint32_t wv = wvals[s];
             wkeys[s] = kEmpty;
             wvals[s] = 0;
-            fd_emit(a, key, wv, upd, &s_min);
+            fd_emit(a, key, wv, upd, band);
           }
         }
         __syncwarp();
       }
       __syncthreads();
       // (5) medium / heavy: whole CTA per vertex
-      for (uint32_t j = 0; j < nsel; j++) {
+      const uint32_t nbig = s_nbig;
+      for (uint32_t bj = 0; bj < nbig; bj++) {
+        const uint32_t j = a.bigl[lo + bj];
         const uint32_t pb = a.selpb[lo + j];
-        if (pb <= kFdWarpCap) continue;  // uniform
         const uint32_t u = a.sel[lo + j];
         if (pb <= kCtaCap) {
           uint32_t logT = ceil_log2(2 * pb);
@@ -282,7 +345,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
               const uint32_t wv = cvals[s];
               ckeys[s] = kEmpty;
               cvals[s] = 0;
-              fd_emit(a, key, wv, upd, &s_min);
+              fd_emit(a, key, wv, upd, band);
             }
           }
           __syncthreads();
@@ -320,7 +383,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
           const uint32_t nd = s_ndup, nt = s_ntouch;
           for (uint32_t q = threadIdx.x; q < nd; q += blockDim.x) {
             const uint32_t key = hdup[q];
-            fd_emit(a, key, hcnt[key], upd, &s_min);
+            fd_emit(a, key, hcnt[key], upd, band);
           }
           __syncthreads();
           for (uint32_t q = threadIdx.x; q < nt; q += blockDim.x) hcnt[htouch[q]] = 0;

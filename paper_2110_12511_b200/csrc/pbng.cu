@@ -50,6 +50,13 @@ size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kC
 void set_attrs_once() {
   static std::once_flag once;
   std::call_once(once, [] {
+    // keep stream-ordered scratch cached between calls (no re-mapping per decomposition)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     cudaFuncSetAttribute(k_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
@@ -419,11 +426,6 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
 void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st, float& ms_build) {
   const uint32_t np = plan.nparts, nU = S.g.nU;
   cudaEvent_t e0 = r.event();
-  S.nslots = choose_slots(r, nU);
-  S.slot_cnt = r.alloc<uint32_t>((size_t)S.nslots * nU);
-  S.slot_touch = r.alloc<uint32_t>((size_t)S.nslots * nU);
-  S.slot_dup = r.alloc<uint32_t>((size_t)S.nslots * nU);
-  CK(cudaMemsetAsync(S.slot_cnt, 0, (size_t)S.nslots * nU * 4, r.st));
   uint32_t* pcount = r.alloc<uint32_t>(np);
   uint32_t* poff = r.alloc<uint32_t>(np + 1);
   uint32_t* pcur = r.alloc<uint32_t>(np);
@@ -432,16 +434,18 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   uint32_t* members = r.alloc<uint32_t>(nU);
   uint32_t* sel = r.alloc<uint32_t>(nU);
   uint32_t* selpb = r.alloc<uint32_t>(nU);
-  uint8_t* peeled = r.alloc<uint8_t>(nU);
+  uint32_t* fstate = r.alloc<uint32_t>(nU);
+  uint32_t* cand = r.alloc<uint32_t>(nU);
+  uint32_t* bigl = r.alloc<uint32_t>(nU);
   uint64_t* seg = r.alloc<uint64_t>(S.g.m);
-  unsigned long long* fdc = r.alloc<unsigned long long>(3);  // wedges, updates, rounds|ticket
-  uint32_t* misc = r.alloc<uint32_t>(2);                     // ticket, rounds_max
+  unsigned long long* fdc = r.alloc<unsigned long long>(3);  // wedges, updates, steps
+  uint32_t* misc = r.alloc<uint32_t>(3);                     // ticket, rounds_max, heavy count
   CK(cudaMemsetAsync(pcount, 0, (size_t)np * 4, r.st));
   CK(cudaMemsetAsync(pcur, 0, (size_t)np * 4, r.st));
   CK(cudaMemsetAsync(work, 0, (size_t)np * 8, r.st));
-  CK(cudaMemsetAsync(peeled, 0, nU, r.st));
+  CK(cudaMemsetAsync(fstate, 0, (size_t)nU * 4, r.st));
   CK(cudaMemsetAsync(fdc, 0, 24, r.st));
-  CK(cudaMemsetAsync(misc, 0, 8, r.st));
+  CK(cudaMemsetAsync(misc, 0, 12, r.st));
   r.pre(PBNG_K_FD_BUILD);
   k_part_count<<<r.nsm * 4, 256, np * 4, r.st>>>(nU, S.part, np, pcount);
   r.post(PBNG_K_FD_BUILD);
@@ -455,11 +459,21 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   k_part_scatter<<<r.nsm * 8, 256, 0, r.st>>>(nU, S.part, poff, pcur, members);
   r.post(PBNG_K_FD_BUILD);
   r.pre(PBNG_K_FD_BUILD);
-  k_fd_seg<<<r.nsm * 8, 256, np * 8, r.st>>>(nU, S.g.offU, S.g.adjU, S.g.offV, S.adjL, S.part, np, seg, work);
+  k_fd_seg<<<r.nsm * 8, 256, np * 8, r.st>>>(nU, S.g.offU, S.g.adjU, S.g.offV, S.adjL, S.part, np, seg, work,
+                                              misc + 2);
   r.post(PBNG_K_FD_BUILD);
   std::vector<unsigned long long> hwork(np);
+  uint32_t hheavy = 0;
   CK(cudaMemcpyAsync(hwork.data(), work, (size_t)np * 8, cudaMemcpyDeviceToHost, r.st));
+  CK(cudaMemcpyAsync(&hheavy, misc + 2, 4, cudaMemcpyDeviceToHost, r.st));
   CK(cudaStreamSynchronize(r.st));
+  // dense-counter slots only when some FD vertex outgrows the CTA table
+  S.nslots = hheavy ? choose_slots(r, nU) : (uint32_t)r.nsm;
+  const size_t slot_elems = hheavy ? (size_t)S.nslots * nU : 1;
+  S.slot_cnt = r.alloc<uint32_t>(slot_elems);
+  S.slot_touch = r.alloc<uint32_t>(slot_elems);
+  S.slot_dup = r.alloc<uint32_t>(slot_elems);
+  CK(cudaMemsetAsync(S.slot_cnt, 0, slot_elems * 4, r.st));
   // workload-aware scheduling: LPT order
   std::vector<uint32_t> ord(np);
   for (uint32_t i = 0; i < np; i++) ord[i] = i;
@@ -482,7 +496,9 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   a.sel = sel;
   a.selpb = selpb;
   a.s = S.support;
-  a.peeled = peeled;
+  a.state = fstate;
+  a.cand = cand;
+  a.bigl = bigl;
   a.theta = theta;
   a.slot_cnt = S.slot_cnt;
   a.slot_touch = S.slot_touch;
