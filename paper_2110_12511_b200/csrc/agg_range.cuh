@@ -34,6 +34,13 @@ struct Pieces {         // per-CTA global scratch, capacity `cap` pieces
   uint64_t* save;       // cursor at the start of the current window (replay)
   uint32_t* head;       // id at the cursor (0xFFFFFFFF when exhausted)
   uint32_t* srange;     // window attempt that last wrote save[]
+  uint64_t* pedge;      // edge index of the list the piece belongs to
+};
+
+// No second pass (CD peel / one-sided count).
+struct NoPass2 {
+  static constexpr bool kOn = false;
+  __device__ void operator()(uint64_t, unsigned long long) const {}
 };
 
 struct RangeShared {
@@ -77,6 +84,18 @@ __device__ __forceinline__ void dup_insert(RangeSmem& S, RangeShared& sh, uint32
     }
     h = (h + 1) & (kDupSlots - 1);
   }
+}
+
+// Repeats recorded for k in the current window (0 when k occurred once).
+__device__ __forceinline__ uint32_t dup_lookup(const RangeSmem& S, uint32_t k) {
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - 13);
+  for (uint32_t probe = 0; probe <= kDupProbe + 1; probe++) {
+    const unsigned long long cur = S.dup[h];
+    if ((uint32_t)(cur >> 32) == k) return (uint32_t)cur;
+    if (cur == kEmptySlot) return 0;
+    h = (h + 1) & (kDupSlots - 1);
+  }
+  return 0;
 }
 
 // One warp consumes a piece from cursor pk (< ek) while ids < b, marking every
@@ -130,11 +149,15 @@ __device__ __forceinline__ void walk_piece(uint64_t& pk, uint64_t ek, uint32_t a
 // Aggregate w(u, u') over every wedge of u and call emit(u', w) once per
 // distinct partner with w >= 2.  Call with the whole CTA; on entry and exit
 // the bitmap is zero and the repeat table empty.
-template <class L, class Emit>
+//
+// Pass2 (vertex-priority counting, start on the non-peel side): after each
+// window, the wedges of every list piece are walked again and the repeats of
+// their partners summed per list: pass2(edge, Σ (w - 1) over its w >= 2 entries).
+template <class L, class Emit, class Pass2 = NoPass2>
 __device__ __forceinline__ void range_agg_one(const L& lists, uint64_t e0, uint64_t e1, uint32_t u,
                                               uint32_t idspace, const uint32_t* __restrict__ adjL, RangeSmem& S,
                                               const Pieces& pc, RangeShared& sh, Emit& emit,
-                                              unsigned long long* dbg) {
+                                              unsigned long long* dbg, const Pass2& pass2 = Pass2()) {
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), w = tid >> 5, nw = bd >> 5;
   const bool vec = (reinterpret_cast<uintptr_t>(adjL) & 15) == 0;
   if (tid == 0) sh.np = 0;
@@ -153,6 +176,7 @@ __device__ __forceinline__ void range_agg_one(const L& lists, uint64_t e0, uint6
       pc.end[slot + k] = base + (uint64_t)min(len, (k + 1) * kPiece);
       pc.head[slot + k] = 0;  // unknown: the first window's walk finds it
       pc.srange[slot + k] = 0;
+      if (Pass2::kOn) pc.pedge[slot + k] = e;
     }
   }
   __syncthreads();
@@ -207,6 +231,27 @@ __device__ __forceinline__ void range_agg_one(const L& lists, uint64_t e0, uint6
     }
     const bool over = sh.over != 0;
     const uint32_t nd = min(sh.ndup, kDupCap);
+    if (Pass2::kOn && any && !over && nd) {
+      // second walk over this window's wedges: repeats of their partners per list
+      if (tid == 0) sh.next = 0;
+      __syncthreads();
+      for (;;) {
+        uint32_t t = 0;
+        if (ln == 0) t = atomicAdd(&sh.next, 1u);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= np) break;
+        if (pc.srange[t] != rid) continue;
+        const uint64_t p0 = pc.save[t], p1 = pc.pos[t];
+        unsigned long long cs = 0;
+        for (uint64_t q = p0 + ln; q < p1; q += 32) {
+          const uint32_t x = adjL[q];
+          if (x != u) cs += dup_lookup(S, x);
+        }
+        cs = warp_sum(cs);
+        if (ln == 0 && cs) pass2(pc.pedge[t], cs);
+      }
+      __syncthreads();
+    }
     if (any) {
       // clear the window bitmap and drain the repeat table
       const uint32_t nwords = (uint32_t)((b64 - a + 31) >> 5);
@@ -247,7 +292,7 @@ __global__ void __launch_bounds__(kRangeThreads, 1) k_agg_range(AggArgs a) {
   for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
   const uint64_t cap = a.piece_cap;
   const Pieces pc{a.piece_pos + blockIdx.x * cap, a.piece_end + blockIdx.x * cap, a.piece_save + blockIdx.x * cap,
-                  a.piece_head + blockIdx.x * cap, a.piece_srange + blockIdx.x * cap};
+                  a.piece_head + blockIdx.x * cap, a.piece_srange + blockIdx.x * cap, nullptr};
   const uint32_t n = *a.count;
   const CdLists L{a.adjU, a.offV, a.ld};
   unsigned long long upd = 0;

@@ -103,7 +103,8 @@ struct FdLists {  // FD: the segment N_v ∩ U_i of the partition's induced subg
 
 // ---- wedge enumeration ------------------------------------------------------
 // One warp walks the partner lists of up to 32 consecutive edges [we0, we1) of
-// one u.  f(ok, u') is called warp-convergently (ok = lane holds an entry).
+// one u.  f(ok, u', e) is called warp-convergently (ok = lane holds an entry;
+// e = edge index of the list the entry came from).
 //   len >= longlim          : deferred to the CTA (index appended to s_long)
 //   32 <= len < longlim     : whole warp strides the list (coalesced)
 //   len < 32                : flattened over the warp with a shuffle binary
@@ -128,11 +129,12 @@ __device__ __forceinline__ void warp_chunk(const L& lists, uint64_t we0, uint64_
     mid &= mid - 1;
     const uint64_t b = __shfl_sync(kFull, base, j);
     const uint32_t l = __shfl_sync(kFull, len, j);
+    const uint64_t ej = we0 + j;
     for (uint32_t t0 = 0; t0 < l; t0 += 32) {
       const uint32_t t = t0 + ln;
       const bool ok = t < l;
       const uint32_t x = ok ? adjV[b + t] : 0u;
-      f(ok, x);
+      f(ok, x, ej);
     }
   }
   const uint32_t slen = len >= 32 ? 0u : len;
@@ -156,7 +158,7 @@ __device__ __forceinline__ void warp_chunk(const L& lists, uint64_t we0, uint64_
     const uint64_t b = __shfl_sync(kFull, base, j);
     const bool ok = t < total;
     const uint32_t x = ok ? adjV[b + (t - ex)] : 0u;
-    f(ok, x);
+    f(ok, x, we0 + j);
   }
 }
 
@@ -188,12 +190,13 @@ __device__ __forceinline__ void cta_wedges(const L& lists, uint64_t e0, uint64_t
     for (uint32_t i = 0; i < nl; i++) {
       uint64_t base;
       uint32_t len;
-      lists.get(c + s_long[i], base, len);
+      const uint64_t ei = c + s_long[i];
+      lists.get(ei, base, len);
       for (uint32_t t0 = 0; t0 < len; t0 += CH) {
         const uint32_t t = t0 + threadIdx.x;
         const bool ok = t < len;
         const uint32_t x = ok ? adjV[base + t] : 0u;
-        f(ok, x);
+        f(ok, x, ei);
       }
     }
     __syncthreads();

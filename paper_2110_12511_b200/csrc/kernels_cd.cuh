@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
     const uint32_t u = it.x;
     uint32_t logT = ceil_log2(2 * it.y);
     logT = logT < 5 ? 5 : logT;
-    auto f = [&](bool ok, uint32_t x) {
+    auto f = [&](bool ok, uint32_t x, uint64_t) {
       if (ok && x != u) hash_insert(keys, vals, logT, x);
     };
     warp_wedges(L, a.offU[u], a.offU[u + 1], a.adjV, f);

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         const uint32_t u = a.sel[lo + j];
         uint32_t logT = ceil_log2(2 * pb);
         logT = logT < 5 ? 5 : logT;
-        auto f = [&](bool ok, uint32_t x) {
+        auto f = [&](bool ok, uint32_t x, uint64_t) {
           if (ok && x != u) hash_insert(wkeys, wvals, logT, x);
         };
         warp_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, f);
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         if (pb <= kCtaCap) {
           uint32_t logT = ceil_log2(2 * pb);
           logT = logT > 14 ? 14 : logT;
-          auto f = [&](bool ok, uint32_t x) {
+          auto f = [&](bool ok, uint32_t x, uint64_t) {
             if (ok && x != u) hash_insert(ckeys, cvals, logT, x);
           };
           cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_long, &s_nlong, f);
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
             s_ndup = 0;
           }
           __syncthreads();
-          auto f = [&](bool ok, uint32_t x) {
+          auto f = [&](bool ok, uint32_t x, uint64_t) {
             bool first = false, second = false;
             if (ok && x != u) {
               const uint32_t old = atomicAdd(&hcnt[x], 1u);
