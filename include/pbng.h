@@ -15,8 +15,9 @@
  *                V.offsets[V.n + 1] (uint64), V.indices[V.m] (uint32 ids in U)
  *              offsets[0] = 0, non-decreasing, offsets[n] = m; U.m == V.m;
  *              no duplicate edges; the two CSRs are transposes of each other.
- *              Each adjacency list must be sorted ascending (checked by
- *              PBNG_OPT_VALIDATE).
+ *              Adjacency order is free: the library relabels both sides by
+ *              decreasing degree (Alg.1 l.2-5) into internal sorted
+ *              copies and maps results back to the caller's labels.
  *   side       0: peel U (arguments as given); 1: peel V (roles swapped).
  *              "peel side" below means U for side 0 and V for side 1
  *              (tip decomposition peels one vertex set).
@@ -107,13 +108,16 @@ enum {
   PBNG_OPT_NO_DELETE = 2,      /* no dynamic edge deletion during CD (PBNG-) */
   PBNG_OPT_VALIDATE = 4,       /* O(m) CSR precondition check -> PBNG_ERR_GRAPH */
   PBNG_OPT_STATS = 8,          /* count wedges / updates on device (small overhead) */
-  PBNG_OPT_FORCE_RECOUNT = 16  /* test hook: take the re-count branch every CD iteration */
+  PBNG_OPT_FORCE_RECOUNT = 16, /* test hook: take the re-count branch every CD iteration */
+  PBNG_OPT_ONESIDED_COUNT = 32 /* count (and re-count) by one-sided wedge aggregation, W = Σ_v d_v^2
+                                  (P:369-373), instead of vertex-priority counting (Alg.1) */
 };
 
 /* Per-vertex butterfly counts of the peel side:
  *   out_support[u] = sum_{u' != u} C(|N_u ∩ N_u'|, 2)   (= ⋈_u, Table 1)
- * computed by wedge aggregation (Alg.1 per-vertex part,
- * P:417-419).  out_support: device, peel-side n entries. */
+ * computed by vertex-priority counting (Alg.1 pveBcnt, per-vertex part,
+ * P:393-426) on the degree-relabeled graph.  out_support: device, peel-side
+ * n entries. */
 int pbng_count_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_support, void* stream);
 
 /* Tip decomposition of the peel side (tip number θ_u):

@@ -280,6 +280,9 @@ __device__ __forceinline__ void range_agg_one(const L& lists, uint64_t e0, uint6
     if (tid == 0) atomicAdd(&dbg[0], 1ull);
     __syncthreads();
     a = b64;
+    // repeats are dense only in parts of the id space (low ranks = high degree):
+    // widen again once a window used a small part of the table
+    if (width < kWindow && nd < kDupCap / 4) width *= 2;
   }
 }
 

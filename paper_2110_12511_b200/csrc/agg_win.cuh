@@ -1,0 +1,370 @@
+// agg_win.cuh — tier-2 wedge aggregation for starts with more partners than a
+// CTA hash table holds (kCtaCap).  One CTA per start.
+//
+// Partner ids are processed one id WINDOW at a time (kWindow ids): a shared-
+// memory bitmap records first occurrences (one atomicOr per wedge) and a
+// repeat table counts the partners seen again (w >= 2); after the window the
+// repeats are emitted with w = 1 + repeats (the same window scheme as
+// agg_range.cuh, which replaces the paper's per-thread n-element wedge array,
+// P:388-390).  Lists are sorted, so the part of every list inside a window is
+// one contiguous segment.  The segment bounds of all windows are found once per
+// start (one binary search per list and window, all lanes in parallel) and
+// every window's work is the union of its segments, cut into chunks that all
+// warps share: coalesced 16-byte loads, no per-list cursor traffic.  Starts
+// with more than kWinLists lists search their segments window by window.  If a
+// window's repeats overflow the table it is retried in halves.
+#pragma once
+// (included inside namespace pbng by kernels_cd.cuh, after agg_range.cuh)
+
+constexpr uint32_t kWinThreads = 1024;
+constexpr uint32_t kWinLists = 1024;  // lists per batch (bounds precomputed when the start has <= this many)
+constexpr uint32_t kWinChunk = 512;   // entries per warp task
+
+struct WinSmem {
+  uint32_t bits[kBitWords];           // 128 KB bitmap of the window
+  unsigned long long dup[kDupSlots];  // 64 KB repeat table (key << 32 | repeats)
+  uint16_t dslot[kDupCap];            // filled slots of the repeat table
+  uint32_t cpre[kWinLists + 1];       // exclusive prefix of chunk counts of the batch
+  uint32_t segS[kWinLists];           // segment [segS, segT) of each list of the batch
+  uint32_t segT[kWinLists];
+  uint32_t scan[33];
+  unsigned long long ek[64];          // entries per coarse window (first kWinMaxW windows)
+};
+
+struct WinShared {
+  uint32_t over, ndup, next, t;
+  unsigned long long acc;
+};
+
+__device__ __forceinline__ void win_dup_insert(WinSmem& S, WinShared& sh, uint32_t k) {
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - 13);
+  const unsigned long long mine = ((unsigned long long)k << 32) | 1ull;
+  for (uint32_t probe = 0;; probe++) {
+    unsigned long long cur = ((volatile unsigned long long*)S.dup)[h];
+    if ((uint32_t)(cur >> 32) == k) {
+      atomicAdd(reinterpret_cast<uint32_t*>(&S.dup[h]), 1u);
+      return;
+    }
+    if (cur == kEmptySlot) {
+      cur = atomicCAS(&S.dup[h], kEmptySlot, mine);
+      if (cur == kEmptySlot) {
+        const uint32_t i = atomicAdd(&sh.ndup, 1u);
+        if (i < kDupCap) S.dslot[i] = (uint16_t)h;
+        else sh.over = 1;
+        return;
+      }
+      if ((uint32_t)(cur >> 32) == k) {
+        atomicAdd(reinterpret_cast<uint32_t*>(&S.dup[h]), 1u);
+        return;
+      }
+    }
+    if (probe >= kDupProbe) {
+      sh.over = 1;
+      return;
+    }
+    h = (h + 1) & (kDupSlots - 1);
+  }
+}
+
+__device__ __forceinline__ uint32_t win_dup_lookup(const WinSmem& S, uint32_t k) {
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - 13);
+  for (uint32_t probe = 0; probe <= kDupProbe + 1; probe++) {
+    const unsigned long long cur = S.dup[h];
+    if ((uint32_t)(cur >> 32) == k) return (uint32_t)cur;
+    if (cur == kEmptySlot) return 0;
+    h = (h + 1) & (kDupSlots - 1);
+  }
+  return 0;
+}
+
+// first index in p[lo, hi) with p[i] >= key
+__device__ __forceinline__ uint32_t lb_range(const uint32_t* __restrict__ p, uint32_t lo, uint32_t hi, uint32_t key) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Mark the entries p[i0, i1) (all inside the window starting at `a`) in the
+// bitmap; repeats go to the table.  Whole warp, 16-byte loads where aligned.
+__device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
+                                         uint32_t skip, WinSmem& S, WinShared& sh) {
+  const uint32_t ln = lane_id();
+  auto one = [&](uint32_t x) {
+    if (x != skip) {
+      const uint32_t o = x - a;
+      const uint32_t bit = 1u << (o & 31);
+      if (atomicOr(&S.bits[o >> 5], bit) & bit) win_dup_insert(S, sh, x);
+    }
+  };
+  uint64_t h = (i0 + 3) & ~3ull;  // first 16-byte aligned index
+  if (h > i1) h = i1;
+  if (i0 + ln < h) one(p[i0 + ln]);
+  const uint64_t t = h + ((i1 - h) & ~3ull);  // end of the aligned body
+  for (uint64_t q = h + 4ull * ln; q < t; q += 128) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + q));
+    one(v.x);
+    one(v.y);
+    one(v.z);
+    one(v.w);
+  }
+  if (t + ln < i1) one(p[t + ln]);
+}
+
+// Σ repeats of the entries p[i0, i1) (pass 2 of vertex-priority counting)
+__device__ __forceinline__ unsigned long long win_sum(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1,
+                                                      uint32_t skip, const WinSmem& S) {
+  unsigned long long cs = 0;
+  for (uint64_t q = i0 + lane_id(); q < i1; q += 32) {
+    const uint32_t x = p[q];
+    if (x != skip) cs += win_dup_lookup(S, x);
+  }
+  return warp_sum(cs);
+}
+
+// One pass over the segments in [a, b) of every list (coarse window k): the
+// segments are cut into chunks of kWinChunk entries that warps take
+// dynamically; fn(i0, i1, e) is called by a whole warp for the partner
+// entries [i0, i1) of list e.  Returns whether any entry was visited.
+template <class L, class Fn>
+__device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t nl, bool pre,
+                                         const uint32_t* __restrict__ bnd, uint32_t W, uint32_t k, uint64_t wa,
+                                         uint64_t wb, uint64_t a, uint64_t b, const uint32_t* __restrict__ partner,
+                                         WinSmem& S, WinShared& sh, Fn& fn) {
+  const uint32_t tid = threadIdx.x, ln = lane_id();
+  bool any = false;
+  for (uint64_t bs = 0; bs < nl; bs += kWinLists) {
+    const uint32_t nb = (uint32_t)(nl - bs < kWinLists ? nl - bs : kWinLists);
+    uint32_t nch = 0;
+    if (tid < nb) {
+      const uint64_t i = bs + tid;
+      uint64_t base;
+      uint32_t len;
+      lists.get(e0 + i, base, len);
+      const uint32_t* p = partner + base;
+      uint32_t s, t;
+      if (pre) {
+        const uint32_t c0 = bnd[i * (W + 1) + k], c1 = bnd[i * (W + 1) + k + 1];
+        s = a == wa ? c0 : lb_range(p, c0, c1, (uint32_t)a);
+        t = b == wb ? c1 : lb_range(p, s, c1, (uint32_t)b);
+      } else {
+        s = lb_range(p, 0, len, (uint32_t)a);
+        t = lb_range(p, s, len, (uint32_t)b);
+      }
+      S.segS[tid] = s;
+      S.segT[tid] = t;
+      nch = (t - s + kWinChunk - 1) / kWinChunk;
+    }
+    uint32_t tot;
+    const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
+    if (tid < nb) S.cpre[tid] = cp;
+    if (tid == 0) {
+      S.cpre[nb] = tot;
+      sh.next = 0;
+    }
+    __syncthreads();
+    any |= tot != 0;
+    for (;;) {
+      uint32_t c = 0;
+      if (ln == 0) c = atomicAdd(&sh.next, 1u);
+      c = __shfl_sync(kFull, c, 0);
+      if (c >= tot) break;
+      uint32_t lo = 0, hi = nb;  // list lo: cpre[lo] <= c < cpre[lo + 1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (S.cpre[mid] <= c) lo = mid; else hi = mid;
+      }
+      uint64_t base;
+      uint32_t len;
+      lists.get(e0 + bs + lo, base, len);
+      const uint64_t i0 = base + S.segS[lo] + (uint64_t)(c - S.cpre[lo]) * kWinChunk;
+      const uint64_t i1e = base + S.segT[lo];
+      fn(i0, i0 + kWinChunk < i1e ? i0 + kWinChunk : i1e, e0 + bs + lo);
+    }
+    __syncthreads();
+  }
+  return any;
+}
+
+// Dense sub-window: 16-bit counters (two per word) over kDenseIds ids, or
+// 32-bit counters over kDenseIds / 2 ids when a start has >= 2^16 lists
+// (w <= number of lists).
+constexpr uint32_t kDenseIds = kBitWords * 2;
+constexpr uint64_t kDenseEntries = 1u << 16;  // coarse windows with more entries go dense
+constexpr uint32_t kWinMaxW = 64;              // windows whose entry counts are kept in shared memory
+
+__device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
+                                           uint32_t skip, bool wide, uint32_t* cnt) {
+  for (uint64_t q = i0 + lane_id(); q < i1; q += 32) {
+    const uint32_t x = p[q];
+    if (x != skip) {
+      const uint32_t o = x - a;
+      if (wide) atomicAdd(&cnt[o], 1u);
+      else atomicAdd(&cnt[o >> 1], 1u << ((o & 1) << 4));
+    }
+  }
+}
+__device__ __forceinline__ uint32_t dense_get(const uint32_t* cnt, uint32_t o, bool wide) {
+  return wide ? cnt[o] : (cnt[o >> 1] >> ((o & 1) << 4)) & 0xFFFFu;
+}
+
+// Aggregate w(start, x) over all wedges of one start (lists e in [e0, e1),
+// partner ids x < idspace, x != skip) and call emit(x, w) for every x with
+// w >= 2; with Pass2, pass2(e, Σ (w - 1)) over the entries of list e (chunk-wise
+// partial sums).  Whole CTA; bitmap zero and table empty on entry and exit.
+// bnd: per-CTA scratch of kWinLists * (wmax + 1) entries.
+// A coarse window with many entries (or whose repeats overflow the table) is
+// counted densely in sub-windows instead of bitmap + repeat table.
+template <class L, class Emit, class Pass2 = NoPass2>
+__device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_t e1, uint32_t skip,
+                                            uint32_t idspace, const uint32_t* __restrict__ partner, WinSmem& S,
+                                            WinShared& sh, uint32_t* __restrict__ bnd, Emit& emit,
+                                            unsigned long long* dbg, const Pass2& pass2 = Pass2()) {
+  const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
+  const uint64_t nl = e1 - e0;
+  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWindow - 1) / kWindow);
+  const bool pre = nl <= kWinLists;
+  const bool wide = nl >= 0xFFFFull;
+  const uint32_t SW = wide ? kDenseIds / 2 : kDenseIds;
+  for (uint32_t k = tid; k < kWinMaxW; k += bd) S.ek[k] = 0;
+  __syncthreads();
+  if (pre) {
+    // bnd[i * (W + 1) + k] = first entry of list i with id >= min(k * kWindow, idspace)
+    for (uint32_t i = wid; i < nl; i += nw) {
+      uint64_t base;
+      uint32_t len;
+      lists.get(e0 + i, base, len);
+      uint32_t prev = 0;
+      for (uint32_t k0 = 0; k0 <= W; k0 += 32) {
+        const uint32_t k = k0 + ln;
+        uint32_t v = 0;
+        if (k <= W) {
+          const uint64_t key = (uint64_t)k * kWindow;
+          v = lb_range(partner + base, 0, len, key < idspace ? (uint32_t)key : idspace);
+          bnd[i * (W + 1) + k] = v;
+        }
+        uint32_t left = __shfl_up_sync(kFull, v, 1);
+        if (ln == 0) left = prev;
+        if (k >= 1 && k <= W && k - 1 < kWinMaxW && v > left) atomicAdd(&S.ek[k - 1], (unsigned long long)(v - left));
+        prev = __shfl_sync(kFull, v, 31);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = 0; k < W; k++) {
+    const uint64_t wa = (uint64_t)k * kWindow;
+    const uint64_t wb = wa + kWindow < idspace ? wa + kWindow : idspace;
+    bool dense = pre && k < kWinMaxW && S.ek[k] > kDenseEntries;
+    if (pre && k < kWinMaxW && S.ek[k] == 0) continue;
+    if (!dense) {
+      // bitmap of first occurrences + repeat table over the whole window
+      if (tid == 0) {
+        sh.over = 0;
+        sh.ndup = 0;
+      }
+      __syncthreads();
+      auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) { win_mark(partner, i0, i1, (uint32_t)wa, skip, S, sh); };
+      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, wa, wb, partner, S, sh, mark);
+      const bool over = sh.over != 0;
+      const uint32_t nd = min(sh.ndup, kDupCap);
+      if (Pass2::kOn && any && !over && nd) {
+        auto sum = [&](uint64_t i0, uint64_t i1, uint64_t e) {
+          const unsigned long long cs = win_sum(partner, i0, i1, skip, S);
+          if (ln == 0 && cs) pass2(e, cs);
+        };
+        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, wa, wb, partner, S, sh, sum);
+      }
+      if (any) {
+        const uint32_t nwords = (uint32_t)((wb - wa + 31) >> 5);
+        for (uint32_t i = tid; i < nwords; i += bd) S.bits[i] = 0;
+        for (uint32_t i = tid; i < nd; i += bd) {
+          const uint32_t sl = S.dslot[i];
+          const unsigned long long v = S.dup[sl];
+          S.dup[sl] = kEmptySlot;
+          if (!over) emit((uint32_t)(v >> 32), (uint32_t)v + 1u);
+        }
+      }
+      if (!over) {
+        if (tid == 0) atomicAdd(&dbg[0], 1ull);
+        __syncthreads();
+        continue;
+      }
+      for (uint32_t i = tid; i < kDupSlots; i += bd) S.dup[i] = kEmptySlot;
+      if (tid == 0) atomicAdd(&dbg[1], 1ull);
+      __syncthreads();
+    }
+    // dense counting in sub-windows of SW ids
+    for (uint64_t a = wa; a < wb; a += SW) {
+      const uint64_t b = a + SW < wb ? a + SW : wb;
+      auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) { dense_mark(partner, i0, i1, (uint32_t)a, skip, wide, S.bits); };
+      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark);
+      if (!any) continue;
+      if (Pass2::kOn) {
+        auto sum = [&](uint64_t i0, uint64_t i1, uint64_t e) {
+          unsigned long long cs = 0;
+          for (uint64_t q = i0 + ln; q < i1; q += 32) {
+            const uint32_t x = partner[q];
+            if (x != skip) cs += dense_get(S.bits, x - (uint32_t)a, wide) - 1u;
+          }
+          cs = warp_sum(cs);
+          if (ln == 0 && cs) pass2(e, cs);
+        };
+        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum);
+      }
+      const uint32_t nwords = wide ? (uint32_t)(b - a) : (uint32_t)((b - a + 1) >> 1);
+      for (uint32_t i = tid; i < nwords; i += bd) {
+        const uint32_t v = S.bits[i];
+        if (v) {
+          S.bits[i] = 0;
+          if (wide) {
+            if (v >= 2) emit((uint32_t)a + i, v);
+          } else {
+            const uint32_t lo = v & 0xFFFFu, hi = v >> 16;
+            if (lo >= 2) emit((uint32_t)a + 2 * i, lo);
+            if (hi >= 2) emit((uint32_t)a + 2 * i + 1, hi);
+          }
+        }
+      }
+      if (tid == 0) atomicAdd(&dbg[2], 1ull);
+      __syncthreads();
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kWinThreads, 1) k_agg_win(AggArgs a) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  WinSmem& S = *reinterpret_cast<WinSmem*>(wsm);
+  __shared__ WinShared sh;
+  for (uint32_t i = threadIdx.x; i < kBitWords; i += blockDim.x) S.bits[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
+  uint32_t* bnd = a.win_bnd + (uint64_t)blockIdx.x * a.win_cap;
+  const uint32_t n = *a.count;
+  const CdLists L{a.adjU, a.offV, a.ld};
+  unsigned long long upd = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      sh.t = atomicAdd(a.ticket, 1u);
+      sh.acc = 0;
+    }
+    __syncthreads();
+    const uint32_t i = sh.t;
+    if (i >= n) break;
+    const uint32_t u = a.list[i].x;
+    uint64_t acc = 0;
+    auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, a.adjV, S, sh, bnd, out, a.c->dbg);
+    if (MODE == 0) {
+      acc = warp_sum(acc);
+      if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);
+      __syncthreads();
+      if (threadIdx.x == 0) a.support[u] = sh.acc;
+    }
+    __syncthreads();
+  }
+  if (MODE == 1) {
+    upd = warp_sum(upd);
+    if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
+  }
+}

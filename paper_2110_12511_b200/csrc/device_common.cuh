@@ -76,6 +76,18 @@ __device__ __forceinline__ void hash_insert(uint32_t* keys, uint32_t* vals, uint
   atomicAdd(&vals[h], 1u);
 }
 
+// Count stored for k by hash_insert (0 if absent).
+__device__ __forceinline__ uint32_t hash_lookup(const uint32_t* keys, const uint32_t* vals, uint32_t logT, uint32_t k) {
+  const uint32_t mask = (1u << logT) - 1;
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - logT);
+  for (;;) {
+    const uint32_t cur = keys[h];
+    if (cur == k) return vals[h];
+    if (cur == kEmpty) return 0;
+    h = (h + 1) & mask;
+  }
+}
+
 // ---- partner-list sources ---------------------------------------------------
 // For edge index e of u (offU[u] <= e < offU[u+1]) give the absolute start of
 // the partner list in adjV and its length.

@@ -16,8 +16,10 @@ constexpr uint32_t kWarpSlots = 1024;           // tier 0: one warp per u
 constexpr uint32_t kWarpCap = kWarpSlots / 2;   // partners bound for tier 0
 constexpr uint32_t kCtaSlots = 16384;           // tier 1: one CTA per u
 constexpr uint32_t kCtaCap = kCtaSlots / 2;     // partners bound for tier 1
+constexpr uint32_t kLogCtaSlots = 14;
 constexpr uint32_t kWarpTierThreads = 256;
 constexpr uint32_t kHeavyThreads = 512;
+constexpr uint32_t kClassBig = 2048;            // classify: degree handled by a whole CTA
 // tier 1: range-partitioned CTA hash (see k_agg_range)
 #ifndef PBNG_RANGE_THREADS
 #define PBNG_RANGE_THREADS 1024
@@ -62,6 +64,8 @@ struct Counters {
   uint32_t nF;                   // frontier size (select)
   uint32_t ntier[3];             // tier list sizes (classify)
   uint32_t ticket[4];            // dynamic work tickets of the aggregation kernels
+  uint32_t nbig;                 // classify: vertices left to k_classify_big
+  uint32_t pad1;
   unsigned long long wedges;     // Σ wl over classified work (traversal, incl. u' = u)
   unsigned long long sel_wc;     // Σ wc over selected (range-target adaptation)
   // managed by the host loop
@@ -96,18 +100,21 @@ __global__ void k_init_v(uint32_t nV, const uint64_t* __restrict__ offV, uint32_
 // Also the most list pieces any u can have (tier-1 cursor scratch size).
 __global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                          const uint64_t* __restrict__ offV, uint64_t* __restrict__ wc,
-                         uint32_t* __restrict__ part, unsigned long long* max_pieces) {
+                         uint32_t* __restrict__ part, unsigned long long* max_pieces,
+                         unsigned long long* sum_min) {
   const uint32_t ln = lane_id();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long mp = 0;
+  unsigned long long mp = 0, smin = 0;
   for (uint64_t u = gw; u < nU; u += nw) {
     uint64_t s = 0, pc = 0;
+    const uint64_t du = offU[u + 1] - offU[u];
     for (uint64_t e = offU[u] + ln; e < offU[u + 1]; e += 32) {
       uint32_t v = adjU[e];
       const uint64_t d = offV[v + 1] - offV[v];
       s += d;
       pc += (d + kPiece - 1) / kPiece;
+      smin += d < du ? d : du;
     }
     s = warp_sum(s);
     pc = warp_sum(pc);
@@ -118,6 +125,8 @@ __global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const u
     }
   }
   if (ln == 0 && mp) atomicMax(max_pieces, mp);
+  smin = warp_sum(smin);
+  if (ln == 0 && smin) atomicAdd(sum_min, smin);
 }
 
 // ---------------------------------------------------------------- classify
@@ -136,20 +145,25 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
                            const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                            const uint32_t* __restrict__ ld, const uint32_t* __restrict__ part,
                            uint64_t* __restrict__ support, uint2* tier0, uint2* tier1, uint2* tier2,
-                           uint32_t* vflag, uint32_t epoch, Counters* c) {
+                           uint2* bigq, uint32_t* vflag, uint32_t epoch, Counters* c) {
   __shared__ unsigned long long s_acc[8][32];  // launched with 256 threads
   const uint32_t ln = lane_id(), wib = threadIdx.x >> 5;
   unsigned long long* acc = s_acc[wib & 7];
   const uint32_t n = list ? *count : nU;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long wsum = 0, ssum = 0, tw[2] = {0, 0};
+  unsigned long long wsum = 0, ssum = 0, tw[3] = {0, 0, 0};
   for (uint64_t b = gw * 32; b < n; b += nw * 32) {
     const uint64_t idx = b + ln;
     bool ok = idx < n;
     const uint32_t u = ok ? (list ? list[idx] : (uint32_t)idx) : 0u;
     if (ok && !list && part[u] != kUnassigned) ok = false;
-    const uint64_t e0 = ok ? offU[u] : 0, d = ok ? offU[u + 1] - e0 : 0;
+    const uint64_t e0 = ok ? offU[u] : 0, d0 = ok ? offU[u + 1] - e0 : 0;
+    // hub vertices are summed by a whole CTA (k_classify_big)
+    const bool big = d0 > kClassBig;
+    warp_append2(big, make_uint2(u, 0), bigq, &c->nbig);
+    if (big) ok = false;
+    const uint64_t d = ok ? d0 : 0;
     acc[ln] = 0;
     // inclusive scan of degrees over the warp (64-bit: a warp may hold hubs)
     uint64_t incl = d;
@@ -198,7 +212,7 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
       if (MODE == 1 && work) work = support[u] != 0;
       if (work) {
         pb = pb64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb64;
-        tier = pb <= kWarpCap ? 0 : 1;
+        tier = pb <= kWarpCap ? 0 : pb <= kCtaCap ? 1 : 2;
         wsum += s;
         ssum += d;
         tw[tier] += s;
@@ -209,18 +223,67 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
     const uint2 item = make_uint2(u, pb);
     warp_append2(tier == 0, item, tier0, &c->ntier[0]);
     warp_append2(tier == 1, item, tier1, &c->ntier[1]);
+    warp_append2(tier == 2, item, tier2, &c->ntier[2]);
     __syncwarp();
   }
   wsum = warp_sum(wsum);
   ssum = warp_sum(ssum);
   tw[0] = warp_sum(tw[0]);
   tw[1] = warp_sum(tw[1]);
+  tw[2] = warp_sum(tw[2]);
   if (ln == 0 && wsum) {
     atomicAdd(&c->wedges, wsum);
     atomicAdd(&c->cum_wedges, wsum);
     atomicAdd(&c->cum_steps, ssum);
     if (tw[0]) atomicAdd(&c->tier_wedges[0], tw[0]);
     if (tw[1]) atomicAdd(&c->tier_wedges[1], tw[1]);
+    if (tw[2]) atomicAdd(&c->tier_wedges[2], tw[2]);
+  }
+}
+
+// The vertices k_classify deferred (degree > kClassBig): one CTA per vertex.
+template <int MODE>
+__global__ void __launch_bounds__(512) k_classify_big(const uint2* __restrict__ bigq, const Counters* cnt,
+                                                     const uint64_t* __restrict__ offU,
+                                                     const uint32_t* __restrict__ adjU,
+                                                     const uint32_t* __restrict__ ld, uint64_t* __restrict__ support,
+                                                     uint2* tier0, uint2* tier1, uint2* tier2, uint32_t* vflag,
+                                                     uint32_t epoch,
+                                                     Counters* c) {
+  __shared__ unsigned long long s_part[16];
+  const uint32_t n = cnt->nbig;
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t u = bigq[i].x;
+    const uint64_t e0 = offU[u], d = offU[u + 1] - e0;
+    unsigned long long s = 0;
+    for (uint64_t k = threadIdx.x; k < d; k += blockDim.x) {
+      const uint32_t v = adjU[e0 + k];
+      s += ld[v];
+      if (vflag && vflag[v] != epoch) vflag[v] = epoch;
+    }
+    s = warp_sum(s);
+    if (lane_id() == 0) s_part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); w++) s += s_part[w];
+      const uint64_t pb64 = s - d;
+      bool work = d >= 2 && pb64 > 0;
+      if (MODE == 1 && work) work = support[u] != 0;
+      if (work) {
+        const uint32_t pb = pb64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb64;
+        const int tier = pb <= kWarpCap ? 0 : pb <= kCtaSlots / 2 ? 1 : 2;
+        uint2* tl = tier == 0 ? tier0 : tier == 1 ? tier1 : tier2;
+        tl[atomicAdd(&c->ntier[tier], 1u)] = make_uint2(u, pb);
+        atomicAdd(&c->wedges, s);
+        atomicAdd(&c->cum_wedges, s);
+        atomicAdd(&c->cum_steps, (unsigned long long)d);
+        atomicAdd(&c->tier_wedges[tier], s);
+      } else if (MODE == 0) {
+        support[u] = 0;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -249,6 +312,13 @@ struct AggArgs {
   uint32_t* piece_srange;
   uint64_t piece_cap;
   Counters* c;
+  // vertex-priority counting (kernels_vp.cuh)
+  uint64_t* piece_pedge;               // tier 1: list (edge index) of each piece (pass 2)
+  const uint32_t* __restrict__ cutV;   // per v: live entries of N_v ranked above v (Alg.1 l.10)
+  const uint32_t* __restrict__ cutU;   // per u: entries of N_u ranked above u
+  // tier 2 (agg_win.cuh): per-CTA window-bound scratch
+  uint32_t* win_bnd;
+  uint64_t win_cap;
 };
 
 template <int MODE>
@@ -313,6 +383,8 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
 }
 
 #include "agg_range.cuh"
+#include "agg_mid.cuh"
+#include "agg_win.cuh"
 
 // ---------------------------------------------------------------- range pass
 // Partition start (Alg.4 l.5-8): snapshot ⋈^init = support for all
@@ -491,6 +563,126 @@ __global__ void __launch_bounds__(512) k_compact_big(const uint32_t* __restrict_
     if (threadIdx.x == 0) {
       ld[v] = lw;
       atomicAdd(&c->ld2_drop, (unsigned long long)L * L - (unsigned long long)lw * lw);
+    }
+    __syncthreads();
+  }
+}
+
+// Lists of >= `big` entries are compacted by several CTAs: chunks of
+// kCompChunk entries count their live entries (copying the chunk to tmp), a
+// per-list scan places the chunks, and every chunk scatters its entries.
+constexpr uint32_t kCompChunk = 4096;
+constexpr uint32_t kCompThreads = 256;
+
+// chunk tasks (touched index, chunk) for every touched list of >= big entries
+__global__ void k_compact_plan(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv,
+                               const uint32_t* __restrict__ ld, uint32_t big, uint2* __restrict__ tasks,
+                               uint32_t* __restrict__ tbase, uint32_t* __restrict__ oldL, uint32_t* ntask) {
+  const uint32_t n = *ntv;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t L = ld[tv[i]];
+    oldL[i] = L;
+    if (L < big) continue;
+    const uint32_t nch = (L + kCompChunk - 1) / kCompChunk;
+    const uint32_t b = atomicAdd(ntask, nch);
+    tbase[i] = b;
+    oldL[i] = L;
+    for (uint32_t k = 0; k < nch; k++) tasks[b + k] = make_uint2(i, k);
+  }
+}
+
+// per chunk: copy to tmp, count live entries -> cnt[task]
+__global__ void __launch_bounds__(kCompThreads) k_compact_count(const uint2* __restrict__ tasks, const uint32_t* ntask,
+                                                                const uint32_t* __restrict__ tv,
+                                                                const uint32_t* __restrict__ oldL,
+                                                                const uint64_t* __restrict__ offV,
+                                                                const uint32_t* __restrict__ adjL, uint32_t* tmp,
+                                                                const uint32_t* __restrict__ part, uint32_t* cnt) {
+  __shared__ uint32_t s_c;
+  const uint32_t nt = *ntask;
+  for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const uint2 tk = tasks[t];
+    const uint64_t base = offV[tv[tk.x]];
+    const uint32_t L = oldL[tk.x];
+    const uint32_t a = tk.y * kCompChunk, b = min(L, a + kCompChunk);
+    if (threadIdx.x == 0) s_c = 0;
+    __syncthreads();
+    uint32_t live = 0;
+    for (uint32_t q = a + threadIdx.x; q < b; q += blockDim.x) {
+      const uint32_t x = adjL[base + q];
+      tmp[base + q] = x;
+      live += part[x] == kUnassigned;
+    }
+    live = warp_sum(live);
+    if (lane_id() == 0 && live) atomicAdd(&s_c, live);
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[t] = s_c;
+    __syncthreads();
+  }
+}
+
+// per big list: exclusive scan of its chunk counts (in place), new live degree
+__global__ void k_compact_scan(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv, uint32_t big,
+                               const uint32_t* __restrict__ tbase, const uint32_t* __restrict__ oldL, uint32_t* cnt,
+                               uint32_t* ld, Counters* c) {
+  const uint32_t n = *ntv;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = tv[i];
+    if (oldL[i] < big) continue;
+    const uint32_t L = oldL[i], b = tbase[i], nch = (L + kCompChunk - 1) / kCompChunk;
+    uint32_t run = 0;
+    for (uint32_t k = 0; k < nch; k++) {
+      const uint32_t x = cnt[b + k];
+      cnt[b + k] = run;
+      run += x;
+    }
+    ld[v] = run;
+    atomicAdd(&c->ld2_drop, (unsigned long long)L * L - (unsigned long long)run * run);
+  }
+}
+
+// per chunk: live entries to [base + live before), peeled ones after the new
+// live prefix (this iteration's peeled group; order inside it is free)
+__global__ void __launch_bounds__(kCompThreads) k_compact_scatter(const uint2* __restrict__ tasks,
+                                                                  const uint32_t* ntask, const uint32_t* __restrict__ tv,
+                                                                  const uint32_t* __restrict__ oldL,
+                                                                  const uint32_t* __restrict__ tbase,
+                                                                  const uint32_t* __restrict__ cnt,
+                                                                  const uint64_t* __restrict__ offV,
+                                                                  const uint32_t* __restrict__ ld, uint32_t* adjL,
+                                                                  const uint32_t* __restrict__ tmp,
+                                                                  const uint32_t* __restrict__ part) {
+  constexpr uint32_t NW = kCompThreads / 32, SL = kCompChunk / NW;  // entries per warp slice
+  __shared__ uint32_t s_w[NW];
+  const uint32_t w = threadIdx.x >> 5, ln = lane_id();
+  const uint32_t nt = *ntask;
+  for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const uint2 tk = tasks[t];
+    const uint32_t v = tv[tk.x];
+    const uint64_t base = offV[v];
+    const uint32_t L = oldL[tk.x], total = ld[v];
+    const uint32_t a = tk.y * kCompChunk, b = min(L, a + kCompChunk);
+    const uint32_t livepre = cnt[t];
+    const uint32_t s0 = a + w * SL, s1 = min(b, s0 + SL);
+    uint32_t lw = 0;
+    for (uint32_t q = s0 + ln; q < s1; q += 32) lw += part[tmp[base + q]] == kUnassigned;
+    lw = warp_sum(lw);
+    if (ln == 0) s_w[w] = lw;
+    __syncthreads();
+    uint32_t lbefore = livepre;
+    for (uint32_t k = 0; k < w; k++) lbefore += s_w[k];
+    uint32_t dbefore = (s0 > b ? b : s0) - lbefore;  // peeled entries before this slice
+    for (uint32_t q0 = s0; q0 < s1; q0 += 32) {
+      const uint32_t q = q0 + ln;
+      const bool ok = q < s1;
+      const uint32_t x = ok ? tmp[base + q] : 0u;
+      const bool live = ok && part[x] == kUnassigned;
+      const bool dead = ok && !live;
+      const uint32_t ml = __ballot_sync(kFull, live), md = __ballot_sync(kFull, dead);
+      if (live) adjL[base + lbefore + __popc(ml & lanemask_lt())] = x;
+      if (dead) adjL[base + total + dbefore + __popc(md & lanemask_lt())] = x;
+      lbefore += __popc(ml);
+      dbefore += __popc(md);
     }
     __syncthreads();
   }

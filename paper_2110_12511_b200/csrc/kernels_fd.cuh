@@ -101,6 +101,16 @@ __global__ void k_fd_seg(uint32_t nU, const uint64_t* __restrict__ offU, const u
 }
 
 // ---------------------------------------------------------------- FD peel
+// One CTA peels one partition level-synchronously (equal to sequential BUP):
+//   level advance: k = max(k, min live support); every live vertex with
+//                  support <= k is selected (θ = k);
+//   cascade:       the selected vertices' wedges decrement their partners;
+//                  a partner whose support drops to <= k ("crosser") is
+//                  selected in the next round at the same level.
+// Crossers are detected by the decrement itself (old > k >= new), so cascade
+// rounds cost O(selected).  Level advances scan a candidate BAND holding every
+// live vertex with support <= T; T is re-chosen from a histogram when the band
+// empties so that the band holds a small share of the partition.
 struct FdArgs {
   uint32_t nU;
   const uint64_t* __restrict__ offU;
@@ -112,13 +122,15 @@ struct FdArgs {
   const uint32_t* __restrict__ order;  // partition ids, decreasing work (LPT)
   uint32_t nparts;
   uint32_t* ticket;
-  uint32_t* members;  // per partition: vertices not yet in the candidate band (compacted at band refills)
-  uint32_t* cand;     // per partition: candidate band C ⊇ {live : support <= T}
-  uint32_t* sel;      // vertices peeled this round
+  uint32_t* members;  // per partition: vertices outside the band (compacted at refills)
+  uint32_t* cand;     // per partition: band, two buffers (cand, cand2)
+  uint32_t* cand2;
+  uint32_t* sel;      // per partition: selected vertices, two buffers (sel, sel2)
+  uint32_t* sel2;
   uint32_t* selpb;    // partner bound per selected vertex (0 = nothing to update)
   uint32_t* bigl;     // indices (into sel) of selected vertices handled by the whole CTA
   uint64_t* s;        // FD supports, initialised to ⋈^init
-  uint32_t* state;    // 0 = in members, 1 = in cand, 2 = peeled
+  uint32_t* state;    // 0 = member, 1 = band, 2 = selected next round, 3 = peeled
   uint64_t* theta;
   uint32_t* slot_cnt;
   uint32_t* slot_touch;
@@ -128,22 +140,31 @@ struct FdArgs {
   uint32_t* rounds_max;
 };
 
-struct FdBand {        // shared-memory view of the partition being peeled
-  uint32_t lo;         // partition offset into members / cand / sel
-  uint32_t nc;         // candidate count (grows when decrements cross T)
-  unsigned long long T;
+struct FdBand {            // shared-memory view of the partition being peeled
+  uint32_t* cand;          // current band buffer (partition slice)
+  uint32_t* next;          // buffer receiving this round's crossers (partition slice)
+  uint32_t nc;             // band entries (grows when decrements cross T)
+  uint32_t nx;             // crossers appended this round
+  unsigned long long T;    // band threshold
+  unsigned long long k;    // level
 };
 
-// s[k] -= C(w,2) for a live partition member; a member of the rest whose
-// support drops to <= T joins the candidate band.
-__device__ __forceinline__ void fd_emit(const FdArgs& a, uint32_t k, uint32_t w, unsigned long long& upd,
+// s[x] -= C(w,2) for a live partition member x; crossers (new <= k) are queued
+// for the next round, members whose support drops to <= T join the band.
+__device__ __forceinline__ void fd_emit(const FdArgs& a, uint32_t x, uint32_t w, unsigned long long& upd,
                                         FdBand& band) {
-  if (w >= 2 && a.state[k] != 2) {
-    const uint64_t d = choose2(w);
-    const uint64_t old = atomicAdd((unsigned long long*)&a.s[k], (unsigned long long)(0ull - d));
-    upd++;
-    if (old - d <= band.T && a.state[k] == 0 && atomicCAS(&a.state[k], 0u, 1u) == 0u)
-      a.cand[band.lo + atomicAdd(&band.nc, 1u)] = k;
+  if (w < 2) return;
+  const uint32_t st = a.state[x];
+  if (st == 3) return;
+  const uint64_t d = choose2(w);
+  const uint64_t nv = atomicAdd((unsigned long long*)&a.s[x], (unsigned long long)(0ull - d)) - d;
+  upd++;
+  if (st == 2) return;
+  if (nv <= band.k) {
+    if (atomicCAS(&a.state[x], st, 2u) == st || (st == 0 && atomicCAS(&a.state[x], 1u, 2u) == 1u))
+      band.next[atomicAdd(&band.nx, 1u)] = x;
+  } else if (st == 0 && nv <= band.T && atomicCAS(&a.state[x], 0u, 1u) == 0u) {
+    band.cand[atomicAdd(&band.nc, 1u)] = x;
   }
 }
 
@@ -155,9 +176,9 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   uint32_t* ckeys = sm + nw * (2 * kFdWarpSlots);
   uint32_t* cvals = ckeys + kCtaSlots;
   uint32_t* s_long = cvals + kCtaSlots;
-  __shared__ uint32_t s_scan[33];
-  __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t, s_nbig;
+  __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t, s_nbig, s_n0, s_n1;
   __shared__ unsigned long long s_min;
+  __shared__ uint32_t s_hist[65];
   __shared__ FdBand band;
   for (uint32_t i = threadIdx.x; i < nw * 2 * kFdWarpSlots; i += blockDim.x) sm[i] = (i / kFdWarpSlots) % 2 == 0 ? kEmpty : 0u;
   for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) {
@@ -179,106 +200,161 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
     if (t >= a.nparts) break;
     const uint32_t p = a.order[t];
     const uint32_t lo = a.poff[p];
+    uint32_t* mem = a.members + lo;
+    uint32_t* cbuf[2] = {a.cand + lo, a.cand2 + lo};
+    uint32_t* sbuf[2] = {a.sel + lo, a.sel2 + lo};
+    uint32_t* selpb = a.selpb + lo;
+    uint32_t* bigl = a.bigl + lo;
     uint32_t nrest = a.poff[p + 1] - lo;
-    uint64_t k = 0;
+    uint32_t cb = 0, sb = 0;  // current band / selection buffers
     uint32_t rounds = 0;
     if (threadIdx.x == 0) {
-      band.lo = lo;
+      band.cand = cbuf[0];
+      band.next = sbuf[1];
       band.nc = 0;
+      band.nx = 0;
       band.T = 0;
+      band.k = 0;
     }
     __syncthreads();
     for (;;) {
-      uint32_t nc = band.nc;
-      if (nc == 0) {
-        // (0) candidate band refill: T = m + max(m/8, 8) from the rest's minimum m;
-        //     members with support <= T move to cand, the rest is compacted
+      uint32_t nsel = band.nx;
+      uint32_t* sel;
+      if (nsel) {
+        // ---- cascade round: this level's crossers (already off the band)
+        sb ^= 1;
+        sel = sbuf[sb];
+        for (uint32_t j = threadIdx.x; j < nsel; j += blockDim.x) {
+          const uint32_t u = sel[j];
+          a.state[u] = 3;
+          a.theta[u] = band.k;
+        }
+      } else {
+        // ---- level advance
+        uint32_t nc = band.nc;
+        if (nc == 0) {
+          // band refill: members' minimum m; T from a log histogram of s - m so
+          // that about max(1024, nrest/32) members enter; the rest is compacted
+          if (threadIdx.x == 0) {
+            s_min = ~0ull;
+            s_n0 = 0;
+          }
+          for (uint32_t i = threadIdx.x; i < 65; i += blockDim.x) s_hist[i] = 0;
+          __syncthreads();
+          uint64_t mn = ~0ull;
+          for (uint32_t j = threadIdx.x; j < nrest; j += blockDim.x) {
+            const uint32_t u = mem[j];
+            if (a.state[u] == 0) {
+              const uint64_t v = a.s[u];
+              mn = v < mn ? v : mn;
+            }
+          }
+          mn = warp_min_u64(mn);
+          if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
+          __syncthreads();
+          const uint64_t m = s_min;
+          if (m == ~0ull) break;  // partition done
+          for (uint32_t j = threadIdx.x; j < nrest; j += blockDim.x) {
+            const uint32_t u = mem[j];
+            if (a.state[u] == 0) {
+              const uint64_t dlt = a.s[u] - m;
+              atomicAdd(&s_hist[dlt ? 64 - __clzll((long long)dlt) : 0], 1u);
+            }
+          }
+          __syncthreads();
+          const uint32_t target = nrest / 32 > 1024 ? nrest / 32 : 1024;
+          uint32_t cum = 0, bb = 0;
+          for (; bb < 64; bb++) {
+            cum += s_hist[bb];
+            if (cum >= target) break;
+          }
+          const uint64_t span = bb >= 64 ? ~0ull : (bb == 0 ? 0ull : ((1ull << bb) - 1));
+          const uint64_t T = span > ~0ull - m ? ~0ull : m + span;
+          uint32_t* cur = cbuf[cb];
+          for (uint32_t j0 = 0; j0 < nrest; j0 += blockDim.x) {
+            const uint32_t j = j0 + threadIdx.x;
+            const uint32_t u = j < nrest ? mem[j] : 0u;
+            const bool lv = j < nrest && a.state[u] == 0;
+            const bool in = lv && a.s[u] <= T;
+            if (in) a.state[u] = 1;
+            __syncthreads();  // every read of this tile precedes the in-place writes below
+            warp_append(in, u, cur, &band.nc);
+            warp_append(lv && !in, u, mem, &s_n0);  // in-place: writes trail reads
+            __syncthreads();
+          }
+          nrest = s_n0;
+          if (threadIdx.x == 0) band.T = T;
+          __syncthreads();
+          nc = band.nc;
+        }
+        // level k = max(k, min support over the band) — every live vertex with
+        // support <= T is in the band, so this is the live minimum
+        uint32_t* cur = cbuf[cb];
         if (threadIdx.x == 0) s_min = ~0ull;
         __syncthreads();
-        uint64_t mn = ~0ull;
-        for (uint32_t j = threadIdx.x; j < nrest; j += blockDim.x) {
-          const uint32_t u = a.members[lo + j];
-          if (a.state[u] == 0) {
-            const uint64_t v = a.s[u];
-            mn = v < mn ? v : mn;
+        {
+          uint64_t mn = ~0ull;
+          for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
+            const uint32_t u = cur[j];
+            if (a.state[u] == 1) {
+              const uint64_t v = a.s[u];
+              mn = v < mn ? v : mn;
+            }
           }
+          mn = warp_min_u64(mn);
+          if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
         }
-        mn = warp_min_u64(mn);
-        if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
         __syncthreads();
-        const uint64_t m = s_min;
-        if (m == ~0ull) break;  // partition done
-        const uint64_t gap = (m >> 3) > 8 ? (m >> 3) : 8;
-        const uint64_t T = m > ~0ull - gap ? ~0ull : m + gap;
-        uint32_t nkeep = 0;
-        for (uint32_t c0 = 0; c0 < nrest; c0 += blockDim.x) {
-          const uint32_t j = c0 + threadIdx.x;
-          const uint32_t u = j < nrest ? a.members[lo + j] : 0u;
-          const bool lv = j < nrest && a.state[u] == 0;
-          const bool in = lv && a.s[u] <= T;
-          const bool kp = lv && !in;
-          uint32_t ti, tk;
-          const uint32_t ri = block_excl_scan(in ? 1u : 0u, s_scan, &ti);
-          const uint32_t rk = block_excl_scan(kp ? 1u : 0u, s_scan, &tk);
-          if (in) {
-            a.cand[lo + nc + ri] = u;
-            a.state[u] = 1;
-          }
-          if (kp) a.members[lo + nkeep + rk] = u;
-          nc += ti;
-          nkeep += tk;
+        if (s_min == ~0ull) {  // only stale entries left in the band: refill
+          if (threadIdx.x == 0) band.nc = 0;
+          __syncthreads();
+          continue;
         }
-        nrest = nkeep;
+        const uint64_t kk = s_min > band.k ? s_min : band.k;
+        // select {band : support <= k} (θ = k); the rest moves to the other band buffer
+        sel = sbuf[sb];
+        uint32_t* oth = cbuf[cb ^ 1];
         if (threadIdx.x == 0) {
-          band.nc = nc;
-          band.T = T;
+          s_n0 = 0;
+          s_n1 = 0;
         }
         __syncthreads();
-      }
-      // (1) level k = max(k, min support over the band) — every live vertex
-      //     with support <= T is in the band, so this is the live minimum
-      if (threadIdx.x == 0) s_min = ~0ull;
-      __syncthreads();
-      {
-        uint64_t mn = ~0ull;
-        for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
-          const uint64_t v = a.s[a.cand[lo + j]];
-          mn = v < mn ? v : mn;
+        for (uint32_t j0 = 0; j0 < nc; j0 += blockDim.x) {
+          const uint32_t j = j0 + threadIdx.x;
+          const uint32_t u = j < nc ? cur[j] : 0u;
+          const bool lv = j < nc && a.state[u] == 1;
+          const bool sl = lv && a.s[u] <= kk;
+          if (sl) {
+            a.state[u] = 3;
+            a.theta[u] = kk;
+          }
+          warp_append(sl, u, sel, &s_n0);
+          warp_append(lv && !sl, u, oth, &s_n1);
         }
-        mn = warp_min_u64(mn);
-        if (ln == 0) atomicMin(&s_min, (unsigned long long)mn);
-      }
-      __syncthreads();
-      k = s_min > k ? s_min : k;
-      // (2) select {support <= k} from the band: θ = k; compact the band
-      uint32_t nsel = 0, nkeep = 0;
-      for (uint32_t c0 = 0; c0 < nc; c0 += blockDim.x) {
-        const uint32_t j = c0 + threadIdx.x;
-        const bool ok = j < nc;
-        const uint32_t u = ok ? a.cand[lo + j] : 0u;
-        const bool sl = ok && a.s[u] <= k;
-        const bool kp = ok && !sl;
-        uint32_t ts, tk;
-        const uint32_t rs = block_excl_scan(sl ? 1u : 0u, s_scan, &ts);
-        const uint32_t rk = block_excl_scan(kp ? 1u : 0u, s_scan, &tk);
-        if (sl) {
-          a.sel[lo + nsel + rs] = u;
-          a.theta[u] = k;
-          a.state[u] = 2;
+        __syncthreads();
+        nsel = s_n0;
+        cb ^= 1;
+        if (threadIdx.x == 0) {
+          band.k = kk;
+          band.cand = oth;
+          band.nc = s_n1;
         }
-        if (kp) a.cand[lo + nkeep + rk] = u;
-        nsel += ts;
-        nkeep += tk;
+        if (nsel == 0) {  // only stale entries were left: refill next time
+          __syncthreads();
+          continue;
+        }
       }
       rounds++;
+      __syncthreads();  // every thread has read band.nx / band.nc of this round
       if (threadIdx.x == 0) {
-        band.nc = nkeep;
+        band.next = sbuf[sb ^ 1];
+        band.nx = 0;
         s_nbig = 0;
       }
       __syncthreads();
       // (3) partner bound of each selected vertex inside G_p
       for (uint32_t j = w; j < nsel; j += nw) {
-        const uint32_t u = a.sel[lo + j];
+        const uint32_t u = sel[j];
         const uint64_t e0 = a.offU[u], e1 = a.offU[u + 1];
         uint64_t wl = 0;
         for (uint64_t e = e0 + ln; e < e1; e += 32) {
@@ -297,16 +373,16 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
             wedges += wl;
             steps += d;
           }
-          a.selpb[lo + j] = r;
-          if (r > kFdWarpCap) a.bigl[lo + atomicAdd(&s_nbig, 1u)] = j;  // whole-CTA work, step (5)
+          selpb[j] = r;
+          if (r > kFdWarpCap) bigl[atomicAdd(&s_nbig, 1u)] = j;  // whole-CTA work, step (5)
         }
       }
       __syncthreads();
       // (4) light: one warp per vertex, per-warp table
       for (uint32_t j = w; j < nsel; j += nw) {
-        const uint32_t pb = a.selpb[lo + j];
+        const uint32_t pb = selpb[j];
         if (pb == 0 || pb > kFdWarpCap) continue;
-        const uint32_t u = a.sel[lo + j];
+        const uint32_t u = sel[j];
         uint32_t logT = ceil_log2(2 * pb);
         logT = logT < 5 ? 5 : logT;
         auto f = [&](bool ok, uint32_t x, uint64_t) {
@@ -329,9 +405,9 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       // (5) medium / heavy: whole CTA per vertex
       const uint32_t nbig = s_nbig;
       for (uint32_t bj = 0; bj < nbig; bj++) {
-        const uint32_t j = a.bigl[lo + bj];
-        const uint32_t pb = a.selpb[lo + j];
-        const uint32_t u = a.sel[lo + j];
+        const uint32_t j = bigl[bj];
+        const uint32_t pb = selpb[j];
+        const uint32_t u = sel[j];
         if (pb <= kCtaCap) {
           uint32_t logT = ceil_log2(2 * pb);
           logT = logT > 14 ? 14 : logT;

@@ -15,6 +15,8 @@
 
 #include "../../include/pbng.h"
 #include "kernels_fd.cuh"
+#include "kernels_relabel.cuh"
+#include "kernels_vp.cuh"
 
 using namespace pbng;
 
@@ -44,6 +46,8 @@ constexpr uint64_t kInf = ~0ull;
 
 size_t warp_tier_smem() { return (size_t)(kWarpTierThreads / 32) * 2 * kWarpSlots * 4; }
 size_t range_smem() { return sizeof(RangeSmem); }
+size_t mid_smem() { return sizeof(MidSmem); }
+size_t win_smem() { return sizeof(WinSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
 size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kCtaSlots + kFdThreads) * 4; }
 
@@ -61,6 +65,18 @@ void set_attrs_once() {
     cudaFuncSetAttribute(k_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
     cudaFuncSetAttribute(k_agg_range<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
+    cudaFuncSetAttribute(k_agg_mid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
+    cudaFuncSetAttribute(k_agg_mid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
+    cudaFuncSetAttribute(k_vp_agg_mid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
+    cudaFuncSetAttribute(k_vp_agg_mid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
+    cudaFuncSetAttribute(k_agg_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+    cudaFuncSetAttribute(k_agg_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+    cudaFuncSetAttribute(k_vp_agg_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+    cudaFuncSetAttribute(k_vp_agg_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+    cudaFuncSetAttribute(k_vp_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
+    cudaFuncSetAttribute(k_vp_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
+    cudaFuncSetAttribute(k_vp_agg_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
+    cudaFuncSetAttribute(k_vp_agg_range<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
     cudaFuncSetAttribute(k_range_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem());
     cudaFuncSetAttribute(k_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem());
     cudaGetLastError();
@@ -185,6 +201,158 @@ void validate(Run& r, const Dev& g) {
   if (hb) fail(PBNG_ERR_GRAPH, hb & 1 ? "CSR offsets invalid" : "CSR index out of range");
 }
 
+// ---------------------------------------------------------------- relabeling
+// Priority relabeling (Alg.1 l.2-5), see kernels_relabel.cuh.
+struct SideRank {
+  uint32_t n = 0, dmax = 0;
+  unsigned long long* binoff = nullptr;  // [dmax + 2]: first rank of degree (dmax - key)
+  unsigned long long* edgoff = nullptr;  // [dmax + 2]: first edge of that degree class
+  uint32_t* rank = nullptr;              // caller label -> rank
+  uint32_t* inv = nullptr;               // rank -> caller label
+  uint64_t* offN = nullptr;              // relabeled CSR
+  uint32_t* adjN = nullptr;
+  uint32_t n_gt_small = 0, n_gt_tile = 0, n_gt_fill = 0;  // lists longer than 32 / 4096 / 2048
+};
+
+void scan_u64(Run& r, unsigned long long* a, uint64_t n) {
+  if (!n) return;
+  const uint64_t nt = (n + kScanTile - 1) / kScanTile;
+  uint64_t* ts = r.alloc<uint64_t>(nt);
+  r.pre(PBNG_K_INIT);
+  k_scan_tiles<<<(unsigned)nt, kScanThreads, 0, r.st>>>(n, (uint64_t*)a, ts);
+  r.post(PBNG_K_INIT);
+  r.pre(PBNG_K_INIT);
+  k_scan_top<<<1, kScanThreads, 0, r.st>>>((uint32_t)nt, ts);
+  r.post(PBNG_K_INIT);
+  r.pre(PBNG_K_INIT);
+  k_scan_add<<<r.nsm * 4, 256, 0, r.st>>>(n, (uint64_t*)a, ts);
+  r.post(PBNG_K_INIT);
+}
+
+uint64_t read_u64(Run& r, const unsigned long long* p) {
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, p, 8, cudaMemcpyDeviceToHost, r.st));
+  CK(cudaStreamSynchronize(r.st));
+  return h;
+}
+
+void rank_side(Run& r, uint32_t n, uint64_t m, const uint64_t* off, SideRank& s) {
+  s.n = n;
+  unsigned long long* dm = r.alloc<unsigned long long>(1);
+  CK(cudaMemsetAsync(dm, 0, 8, r.st));
+  r.pre(PBNG_K_INIT);
+  k_deg_max<<<r.nsm * 4, 256, 0, r.st>>>(n, off, dm);
+  r.post(PBNG_K_INIT);
+  s.dmax = (uint32_t)read_u64(r, dm);
+  const uint64_t nb = (uint64_t)s.dmax + 2;
+  s.binoff = r.alloc<unsigned long long>(nb);
+  s.edgoff = r.alloc<unsigned long long>(nb);
+  uint32_t* cursor = r.alloc<uint32_t>(nb);
+  CK(cudaMemsetAsync(s.binoff, 0, nb * 8, r.st));
+  CK(cudaMemsetAsync(s.edgoff, 0, nb * 8, r.st));
+  CK(cudaMemsetAsync(cursor, 0, nb * 4, r.st));
+  r.pre(PBNG_K_INIT);
+  k_deg_hist<<<r.nsm * 8, 256, 0, r.st>>>(n, off, s.dmax, s.binoff, s.edgoff);
+  r.post(PBNG_K_INIT);
+  scan_u64(r, s.binoff, nb);
+  scan_u64(r, s.edgoff, nb);
+  s.rank = r.alloc<uint32_t>(n);
+  s.inv = r.alloc<uint32_t>(n);
+  s.offN = r.alloc<uint64_t>((size_t)n + 1);
+  r.pre(PBNG_K_INIT);
+  k_rank_scatter<<<r.nsm * 8, 256, 0, r.st>>>(n, off, s.dmax, s.binoff, cursor, s.rank, s.inv);
+  r.post(PBNG_K_INIT);
+  r.pre(PBNG_K_INIT);
+  k_rank_offsets<<<r.nsm * 8, 256, 0, r.st>>>(n, m, s.inv, off, s.dmax, s.binoff, s.edgoff, s.offN);
+  r.post(PBNG_K_INIT);
+  s.adjN = r.alloc<uint32_t>(m);
+  // number of lists longer than d: binoff[dmax - d] (d < dmax), else 0
+  auto n_gt = [&](uint32_t d) -> uint32_t { return d < s.dmax ? (uint32_t)read_u64(r, s.binoff + (s.dmax - d)) : 0u; };
+  s.n_gt_small = n_gt(kSortSmall);
+  s.n_gt_tile = n_gt(kSortTile);
+  s.n_gt_fill = n_gt(2048);
+}
+
+void fill_side(Run& r, const uint64_t* off, const uint32_t* adj, const SideRank& s, const uint32_t* rank_other) {
+  if (!s.n) return;
+  r.pre(PBNG_K_INIT);
+  k_relabel_fill<<<r.nsm * 8, 256, 0, r.st>>>(s.n, s.n_gt_fill, s.inv, off, adj, s.offN, rank_other, s.adjN);
+  r.post(PBNG_K_INIT);
+  if (s.n_gt_fill) {
+    r.pre(PBNG_K_INIT);
+    k_relabel_fill_big<<<std::min<uint32_t>(s.n_gt_fill, r.nsm * 4), 512, 0, r.st>>>(s.n_gt_fill, s.inv, off, adj,
+                                                                                     s.offN, rank_other, s.adjN);
+    r.post(PBNG_K_INIT);
+  }
+}
+
+void sort_side(Run& r, const SideRank& s, uint32_t* tmp) {
+  if (!s.n) return;
+  if (s.n > s.n_gt_small) {
+    r.pre(PBNG_K_INIT);
+    k_sort_small<<<r.nsm * 8, 256, 0, r.st>>>(s.n_gt_small, s.n, s.offN, s.adjN);
+    r.post(PBNG_K_INIT);
+  }
+  // lists longer than one tile: chunk tasks, then merge passes
+  std::vector<uint64_t> hoff(s.n_gt_tile + 1);
+  std::vector<ulonglong2> chunks;
+  if (s.n_gt_tile) {
+    CK(cudaMemcpyAsync(hoff.data(), s.offN, hoff.size() * 8, cudaMemcpyDeviceToHost, r.st));
+    CK(cudaStreamSynchronize(r.st));
+    for (uint32_t i = 0; i < s.n_gt_tile; i++)
+      for (uint64_t a = hoff[i]; a < hoff[i + 1]; a += kSortTile)
+        chunks.push_back(make_ulonglong2(a, std::min<uint64_t>(kSortTile, hoff[i + 1] - a)));
+  }
+  ulonglong2* dch = r.alloc<ulonglong2>(chunks.size());
+  if (!chunks.empty())
+    CK(cudaMemcpyAsync(dch, chunks.data(), chunks.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice, r.st));
+  const uint32_t nseg = (s.n_gt_small - s.n_gt_tile) + (uint32_t)chunks.size();
+  if (nseg) {
+    r.pre(PBNG_K_INIT);
+    k_sort_tile<<<std::min<uint32_t>(nseg, r.nsm * 4), kSortThreads, 0, r.st>>>(
+        s.n_gt_tile, s.n_gt_small, s.offN, dch, (uint32_t)chunks.size(), s.adjN);
+    r.post(PBNG_K_INIT);
+  }
+  for (uint64_t run = kSortTile;; run *= 2) {
+    std::vector<ulonglong2> tiles;
+    for (uint32_t i = 0; i < s.n_gt_tile; i++) {
+      const uint64_t len = hoff[i + 1] - hoff[i];
+      if (len <= run) continue;
+      for (uint64_t t = 0; t * kSortTile < len; t++) tiles.push_back(make_ulonglong2(hoff[i], len | (t << 32)));
+    }
+    if (tiles.empty()) break;
+    ulonglong2* dt = r.alloc<ulonglong2>(tiles.size());
+    CK(cudaMemcpyAsync(dt, tiles.data(), tiles.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice, r.st));
+    const uint32_t nt = (uint32_t)tiles.size();
+    r.pre(PBNG_K_INIT);
+    k_merge_pass<<<std::min<uint32_t>(nt, r.nsm * 4), kSortThreads, 0, r.st>>>(dt, nt, run, s.adjN, tmp);
+    r.post(PBNG_K_INIT);
+    r.pre(PBNG_K_INIT);
+    k_copy_tiles<<<std::min<uint32_t>(nt, r.nsm * 4), 512, 0, r.st>>>(dt, nt, tmp, s.adjN);
+    r.post(PBNG_K_INIT);
+    CK(cudaStreamSynchronize(r.st));  // host vector `tiles` must outlive the copy
+  }
+}
+
+// Relabel both sides of g; returns the graph in rank labels (sorted lists).
+Dev relabel(Run& r, const Dev& g, SideRank& RU, SideRank& RV) {
+  rank_side(r, g.nU, g.m, g.offU, RU);
+  rank_side(r, g.nV, g.m, g.offV, RV);
+  if (g.m) {
+    fill_side(r, g.offU, g.adjU, RU, RV.rank);
+    fill_side(r, g.offV, g.adjV, RV, RU.rank);
+    uint32_t* tmp = r.alloc<uint32_t>(g.m);
+    sort_side(r, RU, tmp);
+    sort_side(r, RV, tmp);
+  }
+  Dev h = g;
+  h.offU = RU.offN;
+  h.adjU = RU.adjN;
+  h.offV = RV.offN;
+  h.adjV = RV.adjN;
+  return h;
+}
+
 // Scratch and state of one decomposition.
 struct State {
   Dev g;
@@ -196,7 +364,7 @@ struct State {
   uint64_t* init;     // ⋈^init
   uint32_t* part;
   uint32_t* F;
-  uint2* tier[3];
+  uint2* tier[4];     // aggregation tiers 0-2, [3] = classify's hub queue
   uint32_t* vflag;
   uint32_t* touched;
   Counters* c;
@@ -209,6 +377,19 @@ struct State {
   uint64_t *piece_pos, *piece_end, *piece_save;
   uint32_t* piece_head;
   uint32_t* piece_srange;
+  uint64_t* piece_pedge;
+  uint32_t* win_bnd;  // tier-2 window bounds, win_cap per CTA
+  uint64_t win_cap;
+  // chunked compaction of long lists
+  uint2* comp_task;
+  uint32_t *comp_tbase, *comp_oldL, *comp_cnt, *comp_ntask;
+  // vertex-priority counting (Alg.1)
+  bool vp;
+  uint32_t* cutU;                 // static prefix of N_u ranked above u
+  uint32_t* cutV;                 // live prefix of N_v ranked above v (per count)
+  unsigned long long* sum_min;    // ∧_cnt = Σ_(u,v) min(d_u, d_v)
+  const SideRank* RU;
+  const SideRank* RV;
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -221,35 +402,58 @@ uint32_t choose_slots(const Run& r, uint32_t nU) {
   return (uint32_t)std::max<size_t>(n, 1);
 }
 
-void alloc_state(Run& r, State& S, const Dev& g, bool need_live) {
+void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank& RU, const SideRank& RV, bool vp) {
   S.g = g;
+  S.vp = vp;
+  S.RU = &RU;
+  S.RV = &RV;
   S.ld = r.alloc<uint32_t>(g.nV);
-  S.adjL = need_live ? r.alloc<uint32_t>(g.m) : const_cast<uint32_t*>(g.adjV);
+  // g is the relabeled graph owned by this call: CD deletes from its V lists in place
+  S.adjL = const_cast<uint32_t*>(g.adjV);
   S.tmp = need_live ? r.alloc<uint32_t>(g.m) : nullptr;
+  if (need_live) {
+    const size_t cap = 2 * (g.m / kCompChunk) + 2;
+    S.comp_task = r.alloc<uint2>(cap);
+    S.comp_cnt = r.alloc<uint32_t>(cap);
+    S.comp_tbase = r.alloc<uint32_t>(g.nV);
+    S.comp_oldL = r.alloc<uint32_t>(g.nV);
+    S.comp_ntask = r.alloc<uint32_t>(1);
+  }
   S.wc = r.alloc<uint64_t>(g.nU);
   S.support = r.alloc<uint64_t>(g.nU);
   S.init = need_live ? r.alloc<uint64_t>(g.nU) : nullptr;
   S.part = r.alloc<uint32_t>(g.nU);
   S.F = r.alloc<uint32_t>(g.nU);
-  for (int t = 0; t < 3; t++) S.tier[t] = r.alloc<uint2>(g.nU);
+  for (int t = 0; t < 4; t++) S.tier[t] = r.alloc<uint2>(std::max(g.nU, g.nV));
   S.vflag = r.alloc<uint32_t>(g.nV);
   S.touched = r.alloc<uint32_t>(g.nV);
   S.c = r.alloc<Counters>(1);
   S.hist_w = r.alloc<unsigned long long>(kBins);
   S.hist_n = r.alloc<uint32_t>(kBins);
-  S.sum_d2 = r.alloc<unsigned long long>(1);
+  S.sum_d2 = r.alloc<unsigned long long>(2);
+  S.sum_min = S.sum_d2 + 1;
   CK(cudaMemsetAsync(S.vflag, 0, (size_t)std::max<uint32_t>(g.nV, 1) * 4, r.st));
   CK(cudaMemsetAsync(S.c, 0, sizeof(Counters), r.st));
-  CK(cudaMemsetAsync(S.sum_d2, 0, 8, r.st));
-  if (need_live && g.m) CK(cudaMemcpyAsync(S.adjL, g.adjV, g.m * 4, cudaMemcpyDeviceToDevice, r.st));
+  CK(cudaMemsetAsync(S.sum_d2, 0, 16, r.st));
   r.pre(PBNG_K_INIT);
   k_init_v<<<r.nsm * 4, 256, 0, r.st>>>(g.nV, g.offV, S.ld, S.sum_d2);
   r.post(PBNG_K_INIT);
   unsigned long long* dmax = r.alloc<unsigned long long>(1);
   CK(cudaMemsetAsync(dmax, 0, 8, r.st));
   r.pre(PBNG_K_INIT);
-  k_init_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, g.offV, S.wc, S.part, dmax);
+  k_init_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, g.offV, S.wc, S.part, dmax, S.sum_min);
   r.post(PBNG_K_INIT);
+  S.cutU = S.cutV = nullptr;
+  if (vp) {
+    S.cutU = r.alloc<uint32_t>(g.nU);
+    S.cutV = r.alloc<uint32_t>(g.nV);
+    r.pre(PBNG_K_COUNT_VP);
+    k_vp_cut_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, RV.binoff, RV.dmax, S.cutU);
+    r.post(PBNG_K_COUNT_VP);
+    r.pre(PBNG_K_COUNT_VP);
+    k_vp_vpieces<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, g.offV, g.adjV, g.offU, dmax);
+    r.post(PBNG_K_COUNT_VP);
+  }
   unsigned long long hmax = 0;
   CK(cudaMemcpyAsync(&hmax, dmax, 8, cudaMemcpyDeviceToHost, r.st));
   CK(cudaStreamSynchronize(r.st));
@@ -260,6 +464,10 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live) {
   S.piece_save = r.alloc<uint64_t>(np);
   S.piece_head = r.alloc<uint32_t>(np);
   S.piece_srange = r.alloc<uint32_t>(np);
+  S.piece_pedge = vp ? r.alloc<uint64_t>(np) : nullptr;
+  const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWindow - 1) / kWindow;
+  S.win_cap = (uint64_t)kWinLists * (wmax + 1);
+  S.win_bnd = r.alloc<uint32_t>((size_t)r.nsm * S.win_cap);
 }
 
 AggArgs agg_args(const State& S, int t) {
@@ -282,6 +490,11 @@ AggArgs agg_args(const State& S, int t) {
   a.piece_srange = S.piece_srange;
   a.piece_cap = S.piece_cap;
   a.c = S.c;
+  a.piece_pedge = S.piece_pedge;
+  a.cutV = S.cutV;
+  a.cutU = S.cutU;
+  a.win_bnd = S.win_bnd;
+  a.win_cap = S.win_cap;
   return a;
 }
 
@@ -291,27 +504,80 @@ void launch_agg(Run& r, const State& S) {
   k_agg_warp<MODE><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
   r.post(PBNG_K_AGG_WARP);
   r.pre(PBNG_K_AGG_CTA);
-  k_agg_range<MODE><<<r.nsm * kRangeCtas, kRangeThreads, range_smem(), r.st>>>(agg_args(S, 1));
+  r.post(PBNG_K_AGG_CTA);
+  r.pre(PBNG_K_AGG_CTA);
+  k_agg_mid<MODE><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+  r.post(PBNG_K_AGG_CTA);
+  r.pre(PBNG_K_AGG_CTA);
+  k_agg_win<MODE><<<r.nsm, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
   r.post(PBNG_K_AGG_CTA);
 }
 
 void reset_tiers(Run& r, State& S) {
-  CK(cudaMemsetAsync(&S.c->ntier[0], 0, 7 * sizeof(uint32_t), r.st));  // ntier[3] + ticket[4]
+  CK(cudaMemsetAsync(&S.c->ntier[0], 0, 8 * sizeof(uint32_t), r.st));  // ntier[3] + ticket[4] + nbig
+}
+
+// Vertex-priority count (Alg.1, kernels_vp.cuh) of every unassigned u on the
+// live graph: starts in U, then starts in V; supports accumulate atomically.
+void vp_count_live(Run& r, State& S) {
+  const Dev& g = S.g;
+  CK(cudaMemsetAsync(S.support, 0, (size_t)g.nU * 8, r.st));
+  r.pre(PBNG_K_COUNT_VP);
+  k_vp_cut_v<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, g.offV, S.adjL, S.ld, S.RU->binoff, S.RU->dmax, S.cutV);
+  r.post(PBNG_K_COUNT_VP);
+  // starts in U
+  reset_tiers(r, S);
+  r.pre(PBNG_K_CLASSIFY);
+  k_vp_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(g.nU, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2]);
+  r.post(PBNG_K_CLASSIFY);
+  r.pre(PBNG_K_AGG_WARP);
+  k_vp_agg_warp<0><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
+  r.post(PBNG_K_AGG_WARP);
+  r.pre(PBNG_K_AGG_CTA);
+  k_vp_agg_mid<0><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+  r.post(PBNG_K_AGG_CTA);
+  r.pre(PBNG_K_AGG_CTA);
+  k_vp_agg_win<0><<<r.nsm, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
+  r.post(PBNG_K_AGG_CTA);
+  // starts in V
+  reset_tiers(r, S);
+  r.pre(PBNG_K_CLASSIFY);
+  k_vp_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(g.nV, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2]);
+  r.post(PBNG_K_CLASSIFY);
+  r.pre(PBNG_K_AGG_WARP);
+  k_vp_agg_warp<1><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
+  r.post(PBNG_K_AGG_WARP);
+  r.pre(PBNG_K_AGG_CTA);
+  k_vp_agg_mid<1><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+  r.post(PBNG_K_AGG_CTA);
+  r.pre(PBNG_K_AGG_CTA);
+  k_vp_agg_win<1><<<r.nsm, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
+  r.post(PBNG_K_AGG_CTA);
 }
 
 // Butterfly count of every unassigned u (initial count, and §5.1 re-count).
 void count_live(Run& r, State& S) {
+  if (S.vp) {
+    vp_count_live(r, S);
+    return;
+  }
   reset_tiers(r, S);
   r.pre(PBNG_K_CLASSIFY);
   k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(S.g.nU, nullptr, nullptr, S.g.offU, S.g.adjU, S.ld, S.part,
-                                               S.support, S.tier[0], S.tier[1], S.tier[2], nullptr, 0, S.c);
+                                               S.support, S.tier[0], S.tier[1], S.tier[2], S.tier[3], nullptr, 0,
+                                               S.c);
+  r.post(PBNG_K_CLASSIFY);
+  r.pre(PBNG_K_CLASSIFY);
+  k_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, S.g.offU, S.g.adjU, S.ld, S.support, S.tier[0],
+                                                  S.tier[1], S.tier[2], nullptr, 0, S.c);
   r.post(PBNG_K_CLASSIFY);
   launch_agg<0>(r, S);
 }
 
 void compact(Run& r, State& S, uint32_t epoch) {
-  const uint32_t big = 4096;
+  const uint32_t big = kCompChunk;
   CK(cudaMemsetAsync(&S.c->ntouched, 0, 4, r.st));
+  CK(cudaMemsetAsync(S.comp_ntask, 0, 4, r.st));
   r.pre(PBNG_K_COMPACT);
   k_collect_touched<<<r.nsm * 8, 256, 0, r.st>>>(S.g.nV, S.vflag, epoch, S.touched, S.c);
   r.post(PBNG_K_COMPACT);
@@ -319,9 +585,23 @@ void compact(Run& r, State& S, uint32_t epoch) {
   k_compact<<<r.nsm * 8, 256, 0, r.st>>>(S.touched, &S.c->ntouched, S.g.offV, S.adjL, S.tmp, S.ld, S.part, big,
                                          S.c);
   r.post(PBNG_K_COMPACT);
+  // lists of >= big entries: chunked over CTAs
   r.pre(PBNG_K_COMPACT);
-  k_compact_big<<<r.nsm, 512, 0, r.st>>>(S.touched, &S.c->ntouched, S.g.offV, S.adjL, S.tmp, S.ld, S.part, big,
-                                         S.c);
+  k_compact_plan<<<r.nsm * 2, 256, 0, r.st>>>(S.touched, &S.c->ntouched, S.ld, big, S.comp_task, S.comp_tbase,
+                                              S.comp_oldL, S.comp_ntask);
+  r.post(PBNG_K_COMPACT);
+  r.pre(PBNG_K_COMPACT);
+  k_compact_count<<<r.nsm * 4, kCompThreads, 0, r.st>>>(S.comp_task, S.comp_ntask, S.touched, S.comp_oldL, S.g.offV,
+                                                        S.adjL, S.tmp, S.part, S.comp_cnt);
+  r.post(PBNG_K_COMPACT);
+  r.pre(PBNG_K_COMPACT);
+  k_compact_scan<<<r.nsm, 256, 0, r.st>>>(S.touched, &S.c->ntouched, big, S.comp_tbase, S.comp_oldL, S.comp_cnt,
+                                          S.ld, S.c);
+  r.post(PBNG_K_COMPACT);
+  r.pre(PBNG_K_COMPACT);
+  k_compact_scatter<<<r.nsm * 4, kCompThreads, 0, r.st>>>(S.comp_task, S.comp_ntask, S.touched, S.comp_oldL,
+                                                          S.comp_tbase, S.comp_cnt, S.g.offV, S.ld, S.adjL, S.tmp,
+                                                          S.part);
   r.post(PBNG_K_COMPACT);
 }
 
@@ -336,8 +616,8 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
   const uint32_t nU = S.g.nU;
   std::vector<unsigned long long> hw(kBins);
   std::vector<uint32_t> hn(kBins);
-  unsigned long long sum_d2 = 0;
-  CK(cudaMemcpyAsync(&sum_d2, S.sum_d2, 8, cudaMemcpyDeviceToHost, r.st));
+  unsigned long long sums[2] = {0, 0};  // Σ_v d_v^2, Σ_(u,v) min(d_u, d_v)
+  CK(cudaMemcpyAsync(sums, S.sum_d2, 16, cudaMemcpyDeviceToHost, r.st));
   plan.bounds.assign(1, 0);
   double scale = 1.0;  // two-way adaptive target, second adaptation
   uint32_t epoch = 0;
@@ -389,7 +669,12 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
       r.post(PBNG_K_SELECT);
       r.pre(PBNG_K_CLASSIFY);
       k_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(nU, S.F, &S.c->nF, S.g.offU, S.g.adjU, S.ld, S.part, S.support,
-                                                   S.tier[0], S.tier[1], S.tier[2], S.vflag, epoch, S.c);
+                                                   S.tier[0], S.tier[1], S.tier[2], S.tier[3], S.vflag, epoch,
+                                                   S.c);
+      r.post(PBNG_K_CLASSIFY);
+      r.pre(PBNG_K_CLASSIFY);
+      k_classify_big<1><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, S.g.offU, S.g.adjU, S.ld, S.support,
+                                                      S.tier[0], S.tier[1], S.tier[2], S.vflag, epoch, S.c);
       r.post(PBNG_K_CLASSIFY);
       const Counters hc = r.readback(S.c);
       if (hc.nF == 0) break;
@@ -402,7 +687,9 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         if (del) compact(r, S, epoch);
         continue;
       }
-      const unsigned long long recount_cost = sum_d2 - hc.ld2_drop;  // one-sided re-count cost (g10)
+      // re-count cost (g10): ∧_cnt = Σ min(d_u, d_v) for vertex-priority
+      // counting; the one-sided count costs Σ_v ld_v^2
+      const unsigned long long recount_cost = S.vp ? sums[1] : sums[0] - hc.ld2_drop;
       const bool recount = !(opts & PBNG_OPT_NO_RECOUNT) &&
                            ((opts & PBNG_OPT_FORCE_RECOUNT) || hc.wedges > recount_cost);
       if (recount) {
@@ -436,6 +723,8 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   uint32_t* selpb = r.alloc<uint32_t>(nU);
   uint32_t* fstate = r.alloc<uint32_t>(nU);
   uint32_t* cand = r.alloc<uint32_t>(nU);
+  uint32_t* cand2 = r.alloc<uint32_t>(nU);
+  uint32_t* sel2 = r.alloc<uint32_t>(nU);
   uint32_t* bigl = r.alloc<uint32_t>(nU);
   uint64_t* seg = r.alloc<uint64_t>(S.g.m);
   unsigned long long* fdc = r.alloc<unsigned long long>(3);  // wedges, updates, steps
@@ -498,6 +787,8 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   a.s = S.support;
   a.state = fstate;
   a.cand = cand;
+  a.cand2 = cand2;
+  a.sel2 = sel2;
   a.bigl = bigl;
   a.theta = theta;
   a.slot_cnt = S.slot_cnt;
@@ -569,7 +860,9 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   }
   State S;
   cudaEvent_t t0 = r.event();
-  alloc_state(r, S, g, true);
+  SideRank RU, RV;
+  const Dev gr = relabel(r, g, RU, RV);
+  alloc_state(r, S, gr, true, RU, RV, !(opts & PBNG_OPT_ONESIDED_COUNT));
   count_live(r, S);
   cudaEvent_t t1 = r.event();
   const Counters c0 = r.readback(S.c);
@@ -586,16 +879,24 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   st.ms_count = elapsed(t0, t1);
   st.ms_cd = elapsed(t1, t2);
   if (out.part) {
-    CK(cudaMemcpyAsync(out.part, S.part, (size_t)g.nU * 4, cudaMemcpyDeviceToDevice, r.st));
-    CK(cudaMemcpyAsync(out.init, S.init, (size_t)g.nU * 8, cudaMemcpyDeviceToDevice, r.st));
+    r.pre(PBNG_K_INIT);
+    k_gather<uint32_t><<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.part, out.part);
+    r.post(PBNG_K_INIT);
+    r.pre(PBNG_K_INIT);
+    k_gather<uint64_t><<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.init, out.init);
+    r.post(PBNG_K_INIT);
     for (uint32_t i = 0; i <= P; i++) out.bounds[i] = i < plan.bounds.size() ? plan.bounds[i] : kInf;
     *out.nparts = plan.nparts;
     CK(cudaStreamSynchronize(r.st));
   }
   if (out.tip) {
     float ms_build = 0;
-    run_fd(r, S, plan, out.tip, st, ms_build);
+    uint64_t* theta = r.alloc<uint64_t>(g.nU);
+    run_fd(r, S, plan, theta, st, ms_build);
     st.ms_fd_build = ms_build;
+    r.pre(PBNG_K_INIT);
+    k_gather<uint64_t><<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, theta, out.tip);
+    r.post(PBNG_K_INIT);
   }
   CK(cudaStreamSynchronize(r.st));
   st.launches = r.launches;
@@ -632,9 +933,13 @@ int pbng_count_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_suppo
     if (g.nU == 0) return;
     Run r((cudaStream_t)stream);
     State S;
-    alloc_state(r, S, g, false);
+    SideRank RU, RV;
+    const Dev gr = relabel(r, g, RU, RV);
+    alloc_state(r, S, gr, false, RU, RV, true);
     count_live(r, S);
-    CK(cudaMemcpyAsync(out_support, S.support, (size_t)g.nU * 8, cudaMemcpyDeviceToDevice, r.st));
+    r.pre(PBNG_K_INIT);
+    k_gather<uint64_t><<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.support, out_support);
+    r.post(PBNG_K_INIT);
     CK(cudaStreamSynchronize(r.st));
   });
 }

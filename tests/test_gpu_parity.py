@@ -60,7 +60,7 @@ def test_tip_tiny_corpus(pb, P):
 
 
 @pytest.mark.parametrize("cfg", [1, 2, "2a"])
-@pytest.mark.parametrize("opts", [0, 1, 2, 3, 16, 18])
+@pytest.mark.parametrize("opts", [0, 1, 2, 3, 16, 18, 32, 48, 50])
 def test_tip_configs_options(pb, cfg, opts):
     g, P = gg.config(cfg)
     want = oracle.bup_tip(g)
@@ -171,3 +171,33 @@ def test_validate_rejects_bad_csr(pb):
     assert ei.value.code == pb.ERR_GRAPH
     tip, _ = pb.pbng_tip_decompose(d, 8, opts=pb.OPT_VALIDATE)
     torch.cuda.synchronize()
+
+
+def test_unsorted_adjacency_and_count_paths(pb):
+    """Adjacency order is not a precondition (the library relabels and sorts
+    internal copies); vertex-priority and one-sided counting give the same θ."""
+    g, P = gg.config(1)
+    rng = np.random.default_rng(5)
+    adj_u, adj_v = g.adj_u.copy(), g.adj_v.copy()
+    for off, adj in ((g.off_u, adj_u), (g.off_v, adj_v)):
+        for x in range(len(off) - 1):
+            seg = adj[off[x]:off[x + 1]]
+            rng.shuffle(seg)
+    d = pb.DeviceGraph.from_numpy(g.off_u, adj_u, g.off_v, adj_v)
+    want = oracle.bup_tip(g)
+    assert np.array_equal(pb.as_u64(pb.pbng_count_butterflies(d)), oracle.count(g))
+    for opts in (0, pb.OPT_ONESIDED_COUNT, pb.OPT_ONESIDED_COUNT | pb.OPT_FORCE_RECOUNT, pb.OPT_FORCE_RECOUNT):
+        tip, _ = pb.pbng_tip_decompose(d, P, opts=opts)
+        assert np.array_equal(pb.as_u64(tip), want), opts
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_tip_tiny_corpus_forced_recount(pb, P):
+    """Every CD iteration re-counts by vertex-priority counting on the live graph."""
+    for g in tiny_corpus(60, 3000 + P):
+        d = dev(pb, g)
+        for side, gs in ((0, g), (1, g.swapped())):
+            tip, _ = pb.pbng_tip_decompose(d, P, side=side, opts=pb.OPT_FORCE_RECOUNT)
+            assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs)), (g.name, side, P)
+            tip, _ = pb.pbng_tip_decompose(d, P, side=side, opts=pb.OPT_FORCE_RECOUNT | pb.OPT_NO_DELETE)
+            assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs)), (g.name, side, P)
