@@ -28,9 +28,14 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 
+_CERT = os.path.join(_HERE, "certificate.c")
+
+
 def build_lib(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", _LIB, _SRC])
+    srcs = [_SRC, _CERT]
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(p) for p in srcs):
+        # -fopenmp serves certificate.c only; oracle.c stays single-threaded
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB] + srcs)
     return _LIB
 
 
@@ -55,6 +60,11 @@ def _load():
         _lib.oracle_bup_tip.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
         for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip):
             f.restype = ctypes.c_int
+        _lib.oracle_cert_support_ge.argtypes = base + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                                       ctypes.c_void_p]
+        _lib.oracle_cert_support_ge.restype = ctypes.c_int
+        _lib.oracle_cert_levels.argtypes = base + [ctypes.c_void_p] * 4 + [ctypes.c_uint64, ctypes.c_void_p]
+        _lib.oracle_cert_levels.restype = ctypes.c_int64
     return _lib
 
 
@@ -97,3 +107,51 @@ def bup_tip(g, stats: Stats | None = None) -> np.ndarray:
         raise MemoryError("oracle_bup_tip failed")
     del keep
     return out
+
+
+def cert_support_ge(g, theta, us=None) -> np.ndarray:
+    """Certificate part (A): s_ge(u) = Σ_{u' != u, θ'_u' >= θ'_u} C(w,2) for the listed u (all if None)."""
+    keep, ptrs = _csr(g)
+    th = np.ascontiguousarray(theta, np.uint64)
+    usa = None if us is None else np.ascontiguousarray(us, np.uint32)
+    n = g.nU if usa is None else usa.shape[0]
+    out = np.zeros(n, np.uint64)
+    if _load().oracle_cert_support_ge(g.nU, g.nV, *ptrs, th.ctypes.data, None if usa is None else usa.ctypes.data,
+                                      n, out.ctypes.data):
+        raise MemoryError("oracle_cert_support_ge failed")
+    del keep
+    return out
+
+
+def cert_levels(g, theta, levels=None):
+    """Certificate part (C) for the given levels (all distinct θ' values if None).
+    Returns (number of failing levels, first failing level or None)."""
+    keep, ptrs = _csr(g)
+    th = np.ascontiguousarray(theta, np.uint64)
+    order = np.argsort(th, kind="stable").astype(np.uint32)
+    vals = th[order]
+    uniq, starts = np.unique(vals, return_index=True)
+    ends = np.append(starts[1:], len(vals))
+    if levels is not None:
+        want = np.isin(uniq, np.asarray(levels, np.uint64))
+        uniq, starts, ends = uniq[want], starts[want], ends[want]
+    members = np.concatenate([order[a:b] for a, b in zip(starts, ends)]) if len(uniq) else np.zeros(0, np.uint32)
+    members = np.ascontiguousarray(members, np.uint32)
+    off = np.zeros(len(uniq) + 1, np.uint64)
+    off[1:] = np.cumsum(ends - starts)
+    lev = np.ascontiguousarray(uniq, np.uint64)
+    first = ctypes.c_uint64(0)
+    bad = _load().oracle_cert_levels(g.nU, g.nV, *ptrs, th.ctypes.data, lev.ctypes.data, off.ctypes.data,
+                                     members.ctypes.data if len(members) else None, len(lev), ctypes.byref(first))
+    if bad < 0:
+        raise MemoryError("oracle_cert_levels failed")
+    del keep
+    return int(bad), (int(lev[first.value]) if bad else None)
+
+
+def certify(g, theta) -> bool:
+    """Full exactness certificate: (A) for every u and (C) for every level."""
+    th = np.ascontiguousarray(theta, np.uint64)
+    if not np.all(cert_support_ge(g, th) >= th):
+        return False
+    return cert_levels(g, th)[0] == 0

@@ -138,6 +138,7 @@ struct FdArgs {
   unsigned long long* wedges;
   unsigned long long* updates;
   uint32_t* rounds_max;
+  unsigned long long* ptrace;  // optional: per partition {rounds, wedges, cycles, members} (PBNG_TRACE)
 };
 
 struct FdBand {            // shared-memory view of the partition being peeled
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
     uint32_t nrest = a.poff[p + 1] - lo;
     uint32_t cb = 0, sb = 0;  // current band / selection buffers
     uint32_t rounds = 0;
+    const long long t_start = clock64();
     if (threadIdx.x == 0) {
       band.cand = cbuf[0];
       band.next = sbuf[1];
@@ -469,6 +471,11 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       __syncthreads();
     }
     rounds_max = rounds > rounds_max ? rounds : rounds_max;
+    if (a.ptrace && threadIdx.x == 0) {
+      a.ptrace[4 * p + 0] = rounds;
+      a.ptrace[4 * p + 1] = clock64() - t_start;
+      a.ptrace[4 * p + 3] = a.poff[p + 1] - lo;
+    }
   }
   wedges = warp_sum(wedges);
   upd = warp_sum(upd);

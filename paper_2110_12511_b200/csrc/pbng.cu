@@ -8,6 +8,7 @@
 // kernels_fd.cuh.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -611,7 +612,17 @@ struct Plan {
 };
 
 // Coarse-grained decomposition (Alg.4 structure P:799-816, tip P:982-991).
+struct TraceRow {
+  uint32_t pid, nF, t0, t1, t2;
+  unsigned long long wedges;
+  bool recount;
+  cudaEvent_t a, b;
+};
+
 void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats& st) {
+  // PBNG_TRACE=1: one stderr line per CD iteration (development aid)
+  const bool trace = std::getenv("PBNG_TRACE") != nullptr;
+  std::vector<TraceRow> rows;
   const bool del = !(opts & PBNG_OPT_NO_DELETE);
   const uint32_t nU = S.g.nU;
   std::vector<unsigned long long> hw(kBins);
@@ -692,6 +703,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
       const unsigned long long recount_cost = S.vp ? sums[1] : sums[0] - hc.ld2_drop;
       const bool recount = !(opts & PBNG_OPT_NO_RECOUNT) &&
                            ((opts & PBNG_OPT_FORCE_RECOUNT) || hc.wedges > recount_cost);
+      cudaEvent_t ta = trace ? r.event() : nullptr;
       if (recount) {
         // §5.1: re-compute supports of all remaining vertices
         if (del) compact(r, S, epoch);
@@ -701,12 +713,22 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         launch_agg<1>(r, S);
         if (del) compact(r, S, epoch);
       }
+      if (trace) {
+        TraceRow row{pid, hc.nF, hc.ntier[0], hc.ntier[1], hc.ntier[2], hc.wedges, recount, ta, r.event()};
+        rows.push_back(row);
+      }
     }
     if (!del) compact(r, S, epoch);
     scale = part_wc ? (double)first_wc / (double)part_wc : 1.0;
   }
   plan.nparts = (uint32_t)plan.bounds.size() - 1;
   if (plan.nparts) plan.bounds.back() = kInf;
+  if (trace) {
+    CK(cudaStreamSynchronize(r.st));
+    for (const TraceRow& t : rows)
+      std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu recount=%d ms=%.3f\n", t.pid, t.nF, t.t0,
+                   t.t1, t.t2, t.wedges, (int)t.recount, elapsed(t.a, t.b));
+  }
 }
 
 // Fine-grained decomposition -> theta.
@@ -797,6 +819,12 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   a.wedges = fdc;
   a.updates = fdc + 1;
   a.rounds_max = misc + 1;
+  const bool trace = std::getenv("PBNG_TRACE") != nullptr;
+  a.ptrace = nullptr;
+  if (trace) {
+    a.ptrace = r.alloc<unsigned long long>((size_t)4 * np);
+    CK(cudaMemsetAsync(a.ptrace, 0, (size_t)32 * np, r.st));
+  }
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>({np, (uint32_t)r.nsm, S.nslots}));
   r.pre(PBNG_K_FD);
   k_fd<<<grid, kFdThreads, fd_smem(), r.st>>>(a);
@@ -813,6 +841,13 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   st.uv_steps_fd = hf[2];
   st.updates_fd = hf[1];
   st.fd_rounds_max = hm[1];
+  if (trace) {
+    std::vector<unsigned long long> pt((size_t)4 * np);
+    CK(cudaMemcpy(pt.data(), a.ptrace, pt.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < np; i++)
+      std::fprintf(stderr, "fd part=%u members=%llu rounds=%llu cycles=%llu work=%llu\n", i, pt[4 * i + 3],
+                   pt[4 * i + 0], pt[4 * i + 1], hwork[i]);
+  }
   ms_build = elapsed(e0, e1);
   st.ms_fd = elapsed(e1, e2);
 }

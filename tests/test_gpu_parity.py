@@ -96,8 +96,11 @@ def test_config3_parity(pb):
     tip, st = pb.pbng_tip_decompose(d, P)
     want_sup = oracle.count(g)
     assert np.array_equal(sup, want_sup)
-    assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(g))
+    want = oracle.bup_tip(g)
+    assert np.array_equal(pb.as_u64(tip), want)
     assert st["partitions_used"] > 1
+    part, init, bounds, nparts = pb.pbng_tip_plan(d, P)
+    _check_plan(g, part, init, bounds, nparts, want)
 
 
 def _check_plan(g, part, init, bounds, nparts, theta):
@@ -201,3 +204,42 @@ def test_tip_tiny_corpus_forced_recount(pb, P):
             assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs)), (g.name, side, P)
             tip, _ = pb.pbng_tip_decompose(d, P, side=side, opts=pb.OPT_FORCE_RECOUNT | pb.OPT_NO_DELETE)
             assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs)), (g.name, side, P)
+
+
+def _sample_levels(th, rng, k=64, max_members=2000):
+    vals, counts = np.unique(th, return_counts=True)
+    small = vals[counts <= max_members]
+    pick = rng.choice(small, size=min(k, len(small)), replace=False) if len(small) else np.zeros(0, np.uint64)
+    return np.unique(np.append(pick, vals[-1]))  # plus the top level (densest core)
+
+
+def test_config4_full_certificate(pb):
+    """Config 4 at full size (8M x 3M peel orientation, 30M edges, P=150):
+    sampled butterfly counts against the oracle, and the multi-core exactness
+    certificate (oracle/certificate.c) over every vertex and level."""
+    g, P = gg.config(4)
+    d = dev(pb, g)
+    th = pb.as_u64(pb.pbng_tip_decompose(d, P)[0])
+    sup = pb.as_u64(pb.pbng_count_butterflies(d))
+    rng = np.random.default_rng(44)
+    us = np.sort(rng.choice(g.nU, 20000, replace=False)).astype(np.uint32)
+    assert np.array_equal(sup[us], oracle.count_subset(g, us))
+    assert np.all(th <= sup)
+    assert oracle.certify(g, th)
+
+
+def test_config5_sampled_certificate(pb):
+    """Config 5 at full size (25M x 30M, 300M edges, P=400): sampled counts,
+    certificate (A) on sampled vertices and (C) on sampled levels."""
+    g, P = gg.config(5)
+    d = dev(pb, g)
+    th = pb.as_u64(pb.pbng_tip_decompose(d, P)[0])
+    sup = pb.as_u64(pb.pbng_count_butterflies(d))
+    del d
+    rng = np.random.default_rng(55)
+    us = np.sort(rng.choice(g.nU, 2000, replace=False)).astype(np.uint32)
+    assert np.array_equal(sup[us], oracle.count_subset(g, us))
+    assert np.all(th <= sup)
+    assert np.all(oracle.cert_support_ge(g, th, us) >= th[us])
+    bad, first = oracle.cert_levels(g, th, _sample_levels(th, rng))
+    assert bad == 0, first

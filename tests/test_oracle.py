@@ -136,3 +136,36 @@ def test_empty_and_degenerate():
     assert list(oracle.bup_tip(g)) == [0, 0, 0]
     g = gg.from_edges(0, 0, [])
     assert oracle.bup_tip(g).shape == (0,)
+
+
+def test_certificate_accepts_definition2_and_rejects_mutations():
+    """oracle/certificate.c: accepts the Definition-2 tip numbers
+    (brute force) and rejects every single ±1 mutation of them."""
+    for g in _tiny_corpus(n=120, seed0=9000):
+        want = np.array(brute.tip_by_definition(g), np.uint64)
+        assert oracle.certify(g, want)
+        for u in range(g.nU):
+            for d in (1, -1):
+                if d < 0 and want[u] == 0:
+                    continue
+                bad = want.copy()
+                bad[u] = np.uint64(int(bad[u]) + d)
+                assert not oracle.certify(g, bad), (g.name, u, d)
+
+
+def test_certificate_rejects_random_vectors():
+    rng = np.random.default_rng(3)
+    for g in _tiny_corpus(n=60, seed0=9500):
+        want = np.array(brute.tip_by_definition(g), np.uint64)
+        sup = oracle.count(g)
+        for _ in range(20):
+            cand = rng.integers(0, sup + 2).astype(np.uint64)
+            assert oracle.certify(g, cand) == bool(np.array_equal(cand, want))
+
+
+def test_certificate_on_config1():
+    g, _ = gg.config(1)
+    th = oracle.bup_tip(g)
+    assert oracle.certify(g, th)
+    s_ge = oracle.cert_support_ge(g, th, us=np.arange(0, g.nU, 7))
+    assert np.all(s_ge >= th[::7])
