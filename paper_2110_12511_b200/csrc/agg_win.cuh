@@ -18,7 +18,7 @@
 
 constexpr uint32_t kWinThreads = 1024;
 constexpr uint32_t kWinLists = 1024;  // lists per batch (bounds precomputed when the start has <= this many)
-constexpr uint32_t kWinChunk = 512;   // entries per warp task
+constexpr uint32_t kWinChunk = 128;   // entries per warp task (one 16-byte load per lane)
 
 struct WinSmem {
   uint32_t bits[kBitWords];           // 128 KB bitmap of the window
@@ -27,6 +27,7 @@ struct WinSmem {
   uint32_t cpre[kWinLists + 1];       // exclusive prefix of chunk counts of the batch
   uint32_t segS[kWinLists];           // segment [segS, segT) of each list of the batch
   uint32_t segT[kWinLists];
+  unsigned long long segB[kWinLists]; // partner-array base of each list of the batch
   uint32_t scan[33];
   unsigned long long ek[64];          // entries per coarse window (first kWinMaxW windows)
 };
@@ -154,6 +155,7 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
       }
       S.segS[tid] = s;
       S.segT[tid] = t;
+      S.segB[tid] = base;
       nch = (t - s + kWinChunk - 1) / kWinChunk;
     }
     uint32_t tot;
@@ -175,9 +177,7 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
         const uint32_t mid = (lo + hi) >> 1;
         if (S.cpre[mid] <= c) lo = mid; else hi = mid;
       }
-      uint64_t base;
-      uint32_t len;
-      lists.get(e0 + bs + lo, base, len);
+      const uint64_t base = S.segB[lo];
       const uint64_t i0 = base + S.segS[lo] + (uint64_t)(c - S.cpre[lo]) * kWinChunk;
       const uint64_t i1e = base + S.segT[lo];
       fn(i0, i0 + kWinChunk < i1e ? i0 + kWinChunk : i1e, e0 + bs + lo);
@@ -216,14 +216,19 @@ __device__ __forceinline__ uint32_t dense_get(const uint32_t* cnt, uint32_t o, b
 // bnd: per-CTA scratch of kWinLists * (wmax + 1) entries.
 // A coarse window with many entries (or whose repeats overflow the table) is
 // counted densely in sub-windows instead of bitmap + repeat table.
+// Only coarse windows [g * W / G, (g + 1) * W / G) are processed (a start may
+// be split into G independent window groups when a batch has few starts).
 template <class L, class Emit, class Pass2 = NoPass2>
 __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_t e1, uint32_t skip,
-                                            uint32_t idspace, const uint32_t* __restrict__ partner, WinSmem& S,
-                                            WinShared& sh, uint32_t* __restrict__ bnd, Emit& emit,
-                                            unsigned long long* dbg, const Pass2& pass2 = Pass2()) {
+                                            uint32_t idspace, uint32_t g, uint32_t G,
+                                            const uint32_t* __restrict__ partner, WinSmem& S, WinShared& sh,
+                                            uint32_t* __restrict__ bnd, Emit& emit, unsigned long long* dbg,
+                                            const Pass2& pass2 = Pass2()) {
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
   const uint64_t nl = e1 - e0;
   const uint32_t W = (uint32_t)(((uint64_t)idspace + kWindow - 1) / kWindow);
+  const uint32_t k0 = (uint32_t)((uint64_t)g * W / G), k1 = (uint32_t)((uint64_t)(g + 1) * W / G);
+  if (k0 >= k1) return;
   const bool pre = nl <= kWinLists;
   const bool wide = nl >= 0xFFFFull;
   const uint32_t SW = wide ? kDenseIds / 2 : kDenseIds;
@@ -236,23 +241,23 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       uint32_t len;
       lists.get(e0 + i, base, len);
       uint32_t prev = 0;
-      for (uint32_t k0 = 0; k0 <= W; k0 += 32) {
-        const uint32_t k = k0 + ln;
+      for (uint32_t kb = k0; kb <= k1; kb += 32) {
+        const uint32_t k = kb + ln;
         uint32_t v = 0;
-        if (k <= W) {
+        if (k <= k1) {
           const uint64_t key = (uint64_t)k * kWindow;
           v = lb_range(partner + base, 0, len, key < idspace ? (uint32_t)key : idspace);
           bnd[i * (W + 1) + k] = v;
         }
         uint32_t left = __shfl_up_sync(kFull, v, 1);
         if (ln == 0) left = prev;
-        if (k >= 1 && k <= W && k - 1 < kWinMaxW && v > left) atomicAdd(&S.ek[k - 1], (unsigned long long)(v - left));
+        if (k > k0 && k <= k1 && k - 1 < kWinMaxW && v > left) atomicAdd(&S.ek[k - 1], (unsigned long long)(v - left));
         prev = __shfl_sync(kFull, v, 31);
       }
     }
   }
   __syncthreads();
-  for (uint32_t k = 0; k < W; k++) {
+  for (uint32_t k = k0; k < k1; k++) {
     const uint64_t wa = (uint64_t)k * kWindow;
     const uint64_t wb = wa + kWindow < idspace ? wa + kWindow : idspace;
     bool dense = pre && k < kWinMaxW && S.ek[k] > kDenseEntries;
@@ -340,7 +345,8 @@ __global__ void __launch_bounds__(kWinThreads, 1) k_agg_win(AggArgs a) {
   for (uint32_t i = threadIdx.x; i < kBitWords; i += blockDim.x) S.bits[i] = 0;
   for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
   uint32_t* bnd = a.win_bnd + (uint64_t)blockIdx.x * a.win_cap;
-  const uint32_t n = *a.count;
+  const uint32_t G = a.win_split;
+  const uint64_t n = (uint64_t)*a.count * G;
   const CdLists L{a.adjU, a.offV, a.ld};
   unsigned long long upd = 0;
   for (;;) {
@@ -349,17 +355,17 @@ __global__ void __launch_bounds__(kWinThreads, 1) k_agg_win(AggArgs a) {
       sh.acc = 0;
     }
     __syncthreads();
-    const uint32_t i = sh.t;
-    if (i >= n) break;
-    const uint32_t u = a.list[i].x;
+    const uint32_t t = sh.t;
+    if (t >= n) break;
+    const uint32_t u = a.list[t / G].x;
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
-    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, a.adjV, S, sh, bnd, out, a.c->dbg);
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, out, a.c->dbg);
     if (MODE == 0) {
       acc = warp_sum(acc);
       if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);
       __syncthreads();
-      if (threadIdx.x == 0) a.support[u] = sh.acc;
+      if (threadIdx.x == 0 && sh.acc) red_add_u64(&a.support[u], sh.acc);  // support zeroed by the caller
     }
     __syncthreads();
   }

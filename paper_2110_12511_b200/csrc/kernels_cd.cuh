@@ -319,6 +319,7 @@ struct AggArgs {
   // tier 2 (agg_win.cuh): per-CTA window-bound scratch
   uint32_t* win_bnd;
   uint64_t win_cap;
+  uint32_t win_split;                  // window groups per tier-2 start (>1 for small batches)
 };
 
 template <int MODE>

@@ -19,23 +19,33 @@ constexpr uint32_t kFdWarpSlots = 512;
 constexpr uint32_t kFdWarpCap = kFdWarpSlots / 2;
 
 // ---------------------------------------------------------------- membership
-__global__ void k_part_count(uint32_t nU, const uint32_t* __restrict__ part, uint32_t nparts, uint32_t* pcount) {
+// A vertex with ⋈^init = 0 is in no butterfly of its partition's subgraph: its
+// tip number is 0 (θ <= support) and peeling it decrements nobody, so it is
+// settled here (θ = 0, peeled) and kept out of the FD member lists.
+__global__ void k_part_count(uint32_t nU, const uint32_t* __restrict__ part, const uint64_t* __restrict__ init,
+                             uint32_t nparts, uint32_t* pcount) {
   extern __shared__ uint32_t hc[];
   for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x) hc[i] = 0;
   __syncthreads();
   for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nU; u += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(&hc[part[u]], 1u);
+    if (init[u]) atomicAdd(&hc[part[u]], 1u);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x)
     if (hc[i]) atomicAdd(&pcount[i], hc[i]);
 }
 
 // members grouped by partition: members[poff[p] ..) (order inside a group is free)
-__global__ void k_part_scatter(uint32_t nU, const uint32_t* __restrict__ part, const uint32_t* __restrict__ poff,
-                               uint32_t* pcur, uint32_t* members) {
+__global__ void k_part_scatter(uint32_t nU, const uint32_t* __restrict__ part, const uint64_t* __restrict__ init,
+                               const uint32_t* __restrict__ poff, uint32_t* pcur, uint32_t* members,
+                               uint32_t* __restrict__ state, uint64_t* __restrict__ theta) {
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < nU; b += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t u = b + threadIdx.x;
-    const bool ok = u < nU;
+    bool ok = u < nU;
+    if (ok && init[u] == 0) {
+      state[u] = 3;
+      theta[u] = 0;
+      ok = false;
+    }
     const uint32_t p = ok ? part[u] : 0xFFFFFFFFu;
     const uint32_t peers = __match_any_sync(kFull, p);
     if (ok) {
@@ -219,6 +229,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       band.k = 0;
     }
     __syncthreads();
+    long long ph[4] = {0, 0, 0, 0}, tph = clock64();  // trace: selection, bounds, light, heavy
     for (;;) {
       uint32_t nsel = band.nx;
       uint32_t* sel;
@@ -348,6 +359,11 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       }
       rounds++;
       __syncthreads();  // every thread has read band.nx / band.nc of this round
+      if (a.ptrace) {
+        const long long now = clock64();
+        ph[0] += now - tph;
+        tph = now;
+      }
       if (threadIdx.x == 0) {
         band.next = sbuf[sb ^ 1];
         band.nx = 0;
@@ -358,6 +374,10 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       for (uint32_t j = w; j < nsel; j += nw) {
         const uint32_t u = sel[j];
         const uint64_t e0 = a.offU[u], e1 = a.offU[u + 1];
+        if (a.s[u] == 0) {  // in no butterfly with a live vertex: decrements nobody
+          if (ln == 0) selpb[j] = 0;
+          continue;
+        }
         uint64_t wl = 0;
         for (uint64_t e = e0 + ln; e < e1; e += 32) {
           uint64_t b;
@@ -380,6 +400,11 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         }
       }
       __syncthreads();
+      if (a.ptrace) {
+        const long long now = clock64();
+        ph[1] += now - tph;
+        tph = now;
+      }
       // (4) light: one warp per vertex, per-warp table
       for (uint32_t j = w; j < nsel; j += nw) {
         const uint32_t pb = selpb[j];
@@ -404,6 +429,11 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         __syncwarp();
       }
       __syncthreads();
+      if (a.ptrace) {
+        const long long now = clock64();
+        ph[2] += now - tph;
+        tph = now;
+      }
       // (5) medium / heavy: whole CTA per vertex
       const uint32_t nbig = s_nbig;
       for (uint32_t bj = 0; bj < nbig; bj++) {
@@ -469,12 +499,18 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         }
       }
       __syncthreads();
+      if (a.ptrace) {
+        const long long now = clock64();
+        ph[3] += now - tph;
+        tph = now;
+      }
     }
     rounds_max = rounds > rounds_max ? rounds : rounds_max;
     if (a.ptrace && threadIdx.x == 0) {
-      a.ptrace[4 * p + 0] = rounds;
-      a.ptrace[4 * p + 1] = clock64() - t_start;
-      a.ptrace[4 * p + 3] = a.poff[p + 1] - lo;
+      a.ptrace[8 * p + 0] = rounds;
+      a.ptrace[8 * p + 1] = clock64() - t_start;
+      a.ptrace[8 * p + 3] = a.poff[p + 1] - lo;
+      for (int q = 0; q < 4; q++) a.ptrace[8 * p + 4 + q] = ph[q];
     }
   }
   wedges = warp_sum(wedges);

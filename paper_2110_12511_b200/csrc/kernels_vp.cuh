@@ -389,7 +389,8 @@ __global__ void __launch_bounds__(kWinThreads, 1) k_vp_agg_win(AggArgs a) {
   for (uint32_t i = threadIdx.x; i < kBitWords; i += blockDim.x) S.bits[i] = 0;
   for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
   uint32_t* bnd = a.win_bnd + (uint64_t)blockIdx.x * a.win_cap;
-  const uint32_t n = *a.count;
+  const uint32_t G = a.win_split;
+  const uint64_t n = (uint64_t)*a.count * G;
   const auto L = VpSide<SIDE>::lists(a);
   const uint32_t* __restrict__ partner = VpSide<SIDE>::partners(a);
   for (;;) {
@@ -398,9 +399,9 @@ __global__ void __launch_bounds__(kWinThreads, 1) k_vp_agg_win(AggArgs a) {
       sh.acc = 0;
     }
     __syncthreads();
-    const uint32_t i = sh.t;
-    if (i >= n) break;
-    const uint32_t x = a.list[i].x;
+    const uint32_t t = sh.t;
+    if (t >= n) break;
+    const uint32_t x = a.list[t / G].x;
     uint64_t e0, e1;
     VpSide<SIDE>::range(a, x, e0, e1);
     if (SIDE == 0) {
@@ -412,14 +413,15 @@ __global__ void __launch_bounds__(kWinThreads, 1) k_vp_agg_win(AggArgs a) {
           acc += d;
         }
       };
-      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, partner, S, sh, bnd, out, a.c->dbg);
+      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, out, a.c->dbg);
       acc = warp_sum(acc);
       if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);
       __syncthreads();
       if (threadIdx.x == 0 && sh.acc) red_add_u64(&a.support[x], sh.acc);
     } else {
       auto out = [&](uint32_t, uint32_t) {};
-      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, partner, S, sh, bnd, out, a.c->dbg, VpPass2{a.adjV, a.support});
+      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, out, a.c->dbg,
+                  VpPass2{a.adjV, a.support});
     }
     __syncthreads();
   }

@@ -381,6 +381,7 @@ struct State {
   uint64_t* piece_pedge;
   uint32_t* win_bnd;  // tier-2 window bounds, win_cap per CTA
   uint64_t win_cap;
+  uint32_t win_split = 1;  // window groups per tier-2 start in the next launch
   // chunked compaction of long lists
   uint2* comp_task;
   uint32_t *comp_tbase, *comp_oldL, *comp_cnt, *comp_ntask;
@@ -496,6 +497,7 @@ AggArgs agg_args(const State& S, int t) {
   a.cutU = S.cutU;
   a.win_bnd = S.win_bnd;
   a.win_cap = S.win_cap;
+  a.win_split = S.win_split;
   return a;
 }
 
@@ -518,6 +520,15 @@ void reset_tiers(Run& r, State& S) {
   CK(cudaMemsetAsync(&S.c->ntier[0], 0, 8 * sizeof(uint32_t), r.st));  // ntier[3] + ticket[4] + nbig
 }
 
+// Tier-2 starts are split into window groups when a batch has fewer than two
+// starts per SM, so that small batches still occupy every SM.
+uint32_t pick_split(const Run& r, uint32_t n2, uint32_t idspace) {
+  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWindow - 1) / kWindow);
+  if (n2 == 0 || W <= 1) return 1;
+  const uint32_t want = (2u * (uint32_t)r.nsm + n2 - 1) / n2;
+  return std::max(1u, std::min(want, W));
+}
+
 // Vertex-priority count (Alg.1, kernels_vp.cuh) of every unassigned u on the
 // live graph: starts in U, then starts in V; supports accumulate atomically.
 void vp_count_live(Run& r, State& S) {
@@ -531,6 +542,7 @@ void vp_count_live(Run& r, State& S) {
   r.pre(PBNG_K_CLASSIFY);
   k_vp_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(g.nU, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2]);
   r.post(PBNG_K_CLASSIFY);
+  S.win_split = pick_split(r, r.readback(S.c).ntier[2], g.nU);
   r.pre(PBNG_K_AGG_WARP);
   k_vp_agg_warp<0><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
   r.post(PBNG_K_AGG_WARP);
@@ -545,6 +557,7 @@ void vp_count_live(Run& r, State& S) {
   r.pre(PBNG_K_CLASSIFY);
   k_vp_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(g.nV, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2]);
   r.post(PBNG_K_CLASSIFY);
+  S.win_split = pick_split(r, r.readback(S.c).ntier[2], g.nV);
   r.pre(PBNG_K_AGG_WARP);
   k_vp_agg_warp<1><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
   r.post(PBNG_K_AGG_WARP);
@@ -562,6 +575,7 @@ void count_live(Run& r, State& S) {
     vp_count_live(r, S);
     return;
   }
+  CK(cudaMemsetAsync(S.support, 0, (size_t)S.g.nU * 8, r.st));  // tier 2 accumulates
   reset_tiers(r, S);
   r.pre(PBNG_K_CLASSIFY);
   k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(S.g.nU, nullptr, nullptr, S.g.offU, S.g.adjU, S.ld, S.part,
@@ -572,6 +586,7 @@ void count_live(Run& r, State& S) {
   k_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, S.g.offU, S.g.adjU, S.ld, S.support, S.tier[0],
                                                   S.tier[1], S.tier[2], nullptr, 0, S.c);
   r.post(PBNG_K_CLASSIFY);
+  S.win_split = pick_split(r, r.readback(S.c).ntier[2], S.g.nU);
   launch_agg<0>(r, S);
 }
 
@@ -710,6 +725,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         count_live(r, S);
         st.recounts++;
       } else {
+        S.win_split = pick_split(r, hc.ntier[2], nU);
         launch_agg<1>(r, S);
         if (del) compact(r, S, epoch);
       }
@@ -758,7 +774,7 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   CK(cudaMemsetAsync(fdc, 0, 24, r.st));
   CK(cudaMemsetAsync(misc, 0, 12, r.st));
   r.pre(PBNG_K_FD_BUILD);
-  k_part_count<<<r.nsm * 4, 256, np * 4, r.st>>>(nU, S.part, np, pcount);
+  k_part_count<<<r.nsm * 4, 256, np * 4, r.st>>>(nU, S.part, S.init, np, pcount);
   r.post(PBNG_K_FD_BUILD);
   std::vector<uint32_t> hcount(np), hoff(np + 1);
   CK(cudaMemcpyAsync(hcount.data(), pcount, (size_t)np * 4, cudaMemcpyDeviceToHost, r.st));
@@ -767,7 +783,7 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   for (uint32_t i = 0; i < np; i++) hoff[i + 1] = hoff[i] + hcount[i];
   CK(cudaMemcpyAsync(poff, hoff.data(), (size_t)(np + 1) * 4, cudaMemcpyHostToDevice, r.st));
   r.pre(PBNG_K_FD_BUILD);
-  k_part_scatter<<<r.nsm * 8, 256, 0, r.st>>>(nU, S.part, poff, pcur, members);
+  k_part_scatter<<<r.nsm * 8, 256, 0, r.st>>>(nU, S.part, S.init, poff, pcur, members, fstate, theta);
   r.post(PBNG_K_FD_BUILD);
   r.pre(PBNG_K_FD_BUILD);
   k_fd_seg<<<r.nsm * 8, 256, np * 8, r.st>>>(nU, S.g.offU, S.g.adjU, S.g.offV, S.adjL, S.part, np, seg, work,
@@ -822,8 +838,8 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   const bool trace = std::getenv("PBNG_TRACE") != nullptr;
   a.ptrace = nullptr;
   if (trace) {
-    a.ptrace = r.alloc<unsigned long long>((size_t)4 * np);
-    CK(cudaMemsetAsync(a.ptrace, 0, (size_t)32 * np, r.st));
+    a.ptrace = r.alloc<unsigned long long>((size_t)8 * np);
+    CK(cudaMemsetAsync(a.ptrace, 0, (size_t)64 * np, r.st));
   }
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>({np, (uint32_t)r.nsm, S.nslots}));
   r.pre(PBNG_K_FD);
@@ -842,11 +858,12 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   st.updates_fd = hf[1];
   st.fd_rounds_max = hm[1];
   if (trace) {
-    std::vector<unsigned long long> pt((size_t)4 * np);
+    std::vector<unsigned long long> pt((size_t)8 * np);
     CK(cudaMemcpy(pt.data(), a.ptrace, pt.size() * 8, cudaMemcpyDeviceToHost));
     for (uint32_t i = 0; i < np; i++)
-      std::fprintf(stderr, "fd part=%u members=%llu rounds=%llu cycles=%llu work=%llu\n", i, pt[4 * i + 3],
-                   pt[4 * i + 0], pt[4 * i + 1], hwork[i]);
+      std::fprintf(stderr, "fd part=%u members=%llu rounds=%llu cycles=%llu work=%llu sel=%llu bounds=%llu "
+                   "light=%llu heavy=%llu\n", i, pt[8 * i + 3], pt[8 * i + 0], pt[8 * i + 1], hwork[i],
+                   pt[8 * i + 4], pt[8 * i + 5], pt[8 * i + 6], pt[8 * i + 7]);
   }
   ms_build = elapsed(e0, e1);
   st.ms_fd = elapsed(e1, e2);
