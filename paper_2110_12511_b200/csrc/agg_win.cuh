@@ -16,20 +16,60 @@
 #pragma once
 // (included inside namespace pbng by kernels_cd.cuh, after agg_range.cuh)
 
-constexpr uint32_t kWinThreads = 1024;
-constexpr uint32_t kWinLists = 1024;  // lists per batch (bounds precomputed when the start has <= this many)
-constexpr uint32_t kWinChunk = 128;   // entries per warp task (one 16-byte load per lane)
+#ifndef PBNG_WIN_LOG_IDS
+#define PBNG_WIN_LOG_IDS 20
+#endif
+#ifndef PBNG_WIN_THREADS
+#define PBNG_WIN_THREADS 1024
+#endif
+#ifndef PBNG_WIN_CTAS
+#define PBNG_WIN_CTAS 1
+#endif
+#ifndef PBNG_WIN_LOG_DUP
+#define PBNG_WIN_LOG_DUP 13
+#endif
+constexpr uint32_t kWinThreads = PBNG_WIN_THREADS;
+constexpr uint32_t kWinCtas = PBNG_WIN_CTAS;           // resident CTAs per SM
+constexpr uint32_t kWinLists = PBNG_WIN_THREADS;       // lists per batch (bounds precomputed when the start has <= this many)
+constexpr uint64_t kWinIds = 1ull << PBNG_WIN_LOG_IDS;  // ids per window
+constexpr uint32_t kWinBitWords = (uint32_t)(kWinIds / 32);
+constexpr uint32_t kWinLogDup = PBNG_WIN_LOG_DUP;
+constexpr uint32_t kWinDupSlots = 1u << kWinLogDup;   // repeat table (key << 32 | repeats)
+constexpr uint32_t kWinDupCap = kWinDupSlots / 2;
+#ifndef PBNG_WIN_CHUNK
+#define PBNG_WIN_CHUNK 128
+#endif
+#ifndef PBNG_SEG_DEPTH
+#define PBNG_SEG_DEPTH 1
+#endif
+constexpr int kSegDepth = PBNG_SEG_DEPTH;  // 16-byte loads per lane issued together
+#ifndef PBNG_WIN_FAST
+#define PBNG_WIN_FAST 1
+#endif
+#ifndef PBNG_DENSE_TOUCH
+#define PBNG_DENSE_TOUCH 1
+#endif
+constexpr uint32_t kWinChunk = PBNG_WIN_CHUNK ? PBNG_WIN_CHUNK : 512;  // entries per warp task
+
+// chunk size for a window of `entries` entries (PBNG_WIN_CHUNK = 0: about two
+// chunks per warp, 128..1024; else fixed)
+__device__ __forceinline__ uint32_t win_chunk(unsigned long long entries) {
+  if (PBNG_WIN_CHUNK) return PBNG_WIN_CHUNK;
+  unsigned long long c = (entries / 64 + 127) & ~127ull;
+  return c < 128 ? 128u : (c > 1024 ? 1024u : (uint32_t)c);
+}
 
 struct WinSmem {
-  uint32_t bits[kBitWords];           // 128 KB bitmap of the window
-  unsigned long long dup[kDupSlots];  // 64 KB repeat table (key << 32 | repeats)
-  uint16_t dslot[kDupCap];            // filled slots of the repeat table
+  uint32_t bits[kWinBitWords];           // 128 KB bitmap of the window
+  unsigned long long dup[kWinDupSlots];  // 64 KB repeat table (key << 32 | repeats)
+  uint16_t dslot[kWinDupCap];            // filled slots of the repeat table
   uint32_t cpre[kWinLists + 1];       // exclusive prefix of chunk counts of the batch
   uint32_t segS[kWinLists];           // segment [segS, segT) of each list of the batch
   uint32_t segT[kWinLists];
   unsigned long long segB[kWinLists]; // partner-array base of each list of the batch
   uint32_t scan[33];
-  unsigned long long ek[64];          // entries per coarse window (first kWinMaxW windows)
+  unsigned long long ek[64];          // entries per coarse window (relative to the first window, kWinMaxW)
+  uint32_t ctot[64];                  // chunks per coarse window (fast path)
 };
 
 struct WinShared {
@@ -38,7 +78,7 @@ struct WinShared {
 };
 
 __device__ __forceinline__ void win_dup_insert(WinSmem& S, WinShared& sh, uint32_t k) {
-  uint32_t h = (k * 0x9E3779B1u) >> (32 - 13);
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - kWinLogDup);
   const unsigned long long mine = ((unsigned long long)k << 32) | 1ull;
   for (uint32_t probe = 0;; probe++) {
     unsigned long long cur = ((volatile unsigned long long*)S.dup)[h];
@@ -50,7 +90,7 @@ __device__ __forceinline__ void win_dup_insert(WinSmem& S, WinShared& sh, uint32
       cur = atomicCAS(&S.dup[h], kEmptySlot, mine);
       if (cur == kEmptySlot) {
         const uint32_t i = atomicAdd(&sh.ndup, 1u);
-        if (i < kDupCap) S.dslot[i] = (uint16_t)h;
+        if (i < kWinDupCap) S.dslot[i] = (uint16_t)h;
         else sh.over = 1;
         return;
       }
@@ -63,17 +103,17 @@ __device__ __forceinline__ void win_dup_insert(WinSmem& S, WinShared& sh, uint32
       sh.over = 1;
       return;
     }
-    h = (h + 1) & (kDupSlots - 1);
+    h = (h + 1) & (kWinDupSlots - 1);
   }
 }
 
 __device__ __forceinline__ uint32_t win_dup_lookup(const WinSmem& S, uint32_t k) {
-  uint32_t h = (k * 0x9E3779B1u) >> (32 - 13);
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - kWinLogDup);
   for (uint32_t probe = 0; probe <= kDupProbe + 1; probe++) {
     const unsigned long long cur = S.dup[h];
     if ((uint32_t)(cur >> 32) == k) return (uint32_t)cur;
     if (cur == kEmptySlot) return 0;
-    h = (h + 1) & (kDupSlots - 1);
+    h = (h + 1) & (kWinDupSlots - 1);
   }
   return 0;
 }
@@ -87,30 +127,55 @@ __device__ __forceinline__ uint32_t lb_range(const uint32_t* __restrict__ p, uin
   return lo;
 }
 
+// Visit the entries p[i0, i1) with a whole warp: fn(ok, x) is called
+// warp-convergently (ok = the lane holds an entry).  The 16-byte aligned body is
+// read 512 entries per step, four independent 16-byte loads per lane issued
+// before any entry is used, so each warp keeps 2 KB of loads in flight.
+template <class Fn>
+__device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, Fn& fn) {
+  const uint32_t ln = lane_id();
+  uint64_t h = (i0 + 3) & ~3ull;  // first 16-byte aligned index
+  if (h > i1) h = i1;
+  {
+    const bool ok = i0 + ln < h;
+    fn(ok, ok ? p[i0 + ln] : 0u);
+  }
+  const uint64_t t = h + ((i1 - h) & ~3ull);  // end of the aligned body
+  for (uint64_t q0 = h; q0 < t; q0 += 128 * kSegDepth) {
+    uint4 v[kSegDepth];
+    bool ok[kSegDepth];
+#pragma unroll
+    for (int j = 0; j < kSegDepth; j++) {
+      const uint64_t q = q0 + 128 * j + 4 * ln;
+      ok[j] = q < t;
+      v[j] = ok[j] ? __ldg(reinterpret_cast<const uint4*>(p + q)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kSegDepth; j++) {
+      fn(ok[j], v[j].x);
+      fn(ok[j], v[j].y);
+      fn(ok[j], v[j].z);
+      fn(ok[j], v[j].w);
+    }
+  }
+  {
+    const bool ok = t + ln < i1;
+    fn(ok, ok ? p[t + ln] : 0u);
+  }
+}
+
 // Mark the entries p[i0, i1) (all inside the window starting at `a`) in the
-// bitmap; repeats go to the table.  Whole warp, 16-byte loads where aligned.
+// bitmap; repeats go to the table.
 __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
                                          uint32_t skip, WinSmem& S, WinShared& sh) {
-  const uint32_t ln = lane_id();
-  auto one = [&](uint32_t x) {
-    if (x != skip) {
+  auto one = [&](bool ok, uint32_t x) {
+    if (ok && x != skip) {
       const uint32_t o = x - a;
       const uint32_t bit = 1u << (o & 31);
       if (atomicOr(&S.bits[o >> 5], bit) & bit) win_dup_insert(S, sh, x);
     }
   };
-  uint64_t h = (i0 + 3) & ~3ull;  // first 16-byte aligned index
-  if (h > i1) h = i1;
-  if (i0 + ln < h) one(p[i0 + ln]);
-  const uint64_t t = h + ((i1 - h) & ~3ull);  // end of the aligned body
-  for (uint64_t q = h + 4ull * ln; q < t; q += 128) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + q));
-    one(v.x);
-    one(v.y);
-    one(v.z);
-    one(v.w);
-  }
-  if (t + ln < i1) one(p[t + ln]);
+  seg_visit(p, i0, i1, one);
 }
 
 // Σ repeats of the entries p[i0, i1) (pass 2 of vertex-priority counting)
@@ -132,7 +197,7 @@ template <class L, class Fn>
 __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t nl, bool pre,
                                          const uint32_t* __restrict__ bnd, uint32_t W, uint32_t k, uint64_t wa,
                                          uint64_t wb, uint64_t a, uint64_t b, const uint32_t* __restrict__ partner,
-                                         WinSmem& S, WinShared& sh, Fn& fn) {
+                                         WinSmem& S, WinShared& sh, Fn& fn, uint32_t chunk = kWinChunk) {
   const uint32_t tid = threadIdx.x, ln = lane_id();
   bool any = false;
   for (uint64_t bs = 0; bs < nl; bs += kWinLists) {
@@ -156,7 +221,7 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
       S.segS[tid] = s;
       S.segT[tid] = t;
       S.segB[tid] = base;
-      nch = (t - s + kWinChunk - 1) / kWinChunk;
+      nch = (t - s + chunk - 1) / chunk;
     }
     uint32_t tot;
     const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
@@ -178,9 +243,9 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
         if (S.cpre[mid] <= c) lo = mid; else hi = mid;
       }
       const uint64_t base = S.segB[lo];
-      const uint64_t i0 = base + S.segS[lo] + (uint64_t)(c - S.cpre[lo]) * kWinChunk;
+      const uint64_t i0 = base + S.segS[lo] + (uint64_t)(c - S.cpre[lo]) * chunk;
       const uint64_t i1e = base + S.segT[lo];
-      fn(i0, i0 + kWinChunk < i1e ? i0 + kWinChunk : i1e, e0 + bs + lo);
+      fn(i0, i0 + chunk < i1e ? i0 + chunk : i1e, e0 + bs + lo);
     }
     __syncthreads();
   }
@@ -190,20 +255,37 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
 // Dense sub-window: 16-bit counters (two per word) over kDenseIds ids, or
 // 32-bit counters over kDenseIds / 2 ids when a start has >= 2^16 lists
 // (w <= number of lists).
-constexpr uint32_t kDenseIds = kBitWords * 2;
+constexpr uint32_t kDenseIds = kWinBitWords * 2;
 constexpr uint64_t kDenseEntries = 1u << 16;  // coarse windows with more entries go dense
 constexpr uint32_t kWinMaxW = 64;              // windows whose entry counts are kept in shared memory
 
+// Dense marking: one atomicAdd per wedge; the first increment of a word
+// appends the word to the touched list (kept in the repeat table's memory,
+// which dense mode does not use), so the sweep visits touched words only.
+constexpr uint32_t kTouchCap = kWinDupSlots * 2;
 __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
-                                           uint32_t skip, bool wide, uint32_t* cnt) {
-  for (uint64_t q = i0 + lane_id(); q < i1; q += 32) {
-    const uint32_t x = p[q];
-    if (x != skip) {
+                                           uint32_t skip, bool wide, uint32_t* cnt, uint32_t* touch,
+                                           uint32_t* ntouch) {
+  const uint32_t ln = lane_id();
+  auto one = [&](bool ok, uint32_t x) {
+    bool fresh = false;
+    uint32_t wd = 0;
+    if (ok && x != skip) {
       const uint32_t o = x - a;
-      if (wide) atomicAdd(&cnt[o], 1u);
-      else atomicAdd(&cnt[o >> 1], 1u << ((o & 1) << 4));
+      wd = wide ? o : o >> 1;
+      fresh = atomicAdd(&cnt[wd], wide ? 1u : 1u << ((o & 1) << 4)) == 0u;
     }
-  }
+    const uint32_t m = __ballot_sync(kFull, fresh);
+    if (m) {
+      const uint32_t leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (ln == leader) base = atomicAdd(ntouch, (uint32_t)__popc(m));
+      base = __shfl_sync(kFull, base, leader);
+      const uint32_t slot = base + __popc(m & lanemask_lt());
+      if (fresh && slot < kTouchCap) touch[slot] = wd;
+    }
+  };
+  seg_visit(p, i0, i1, one);
 }
 __device__ __forceinline__ uint32_t dense_get(const uint32_t* cnt, uint32_t o, bool wide) {
   return wide ? cnt[o] : (cnt[o >> 1] >> ((o & 1) << 4)) & 0xFFFFu;
@@ -226,43 +308,115 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
                                             const Pass2& pass2 = Pass2()) {
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
   const uint64_t nl = e1 - e0;
-  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWindow - 1) / kWindow);
+  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
   const uint32_t k0 = (uint32_t)((uint64_t)g * W / G), k1 = (uint32_t)((uint64_t)(g + 1) * W / G);
   if (k0 >= k1) return;
-  const bool pre = nl <= kWinLists;
+  // fast path: every list's window bounds, base and per-window chunk prefixes
+  // are computed once per start (per-CTA scratch), so a window needs no scan
+  const bool pre = nl <= kWinLists && k1 - k0 <= kWinMaxW;
   const bool wide = nl >= 0xFFFFull;
   const uint32_t SW = wide ? kDenseIds / 2 : kDenseIds;
+  const uint32_t W1 = W + 1;
+  uint32_t* cpg = bnd + (uint64_t)kWinLists * W1;                        // [kr * kWinLists + i]
+  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(cpg + (uint64_t)kWinLists * W1);
   for (uint32_t k = tid; k < kWinMaxW; k += bd) S.ek[k] = 0;
   __syncthreads();
   if (pre) {
-    // bnd[i * (W + 1) + k] = first entry of list i with id >= min(k * kWindow, idspace)
+    // bnd[i * (W + 1) + k] = first entry of list i with id >= min(k * kWinIds, idspace)
     for (uint32_t i = wid; i < nl; i += nw) {
       uint64_t base;
       uint32_t len;
       lists.get(e0 + i, base, len);
+      if (ln == 0) gbase[i] = base;
       uint32_t prev = 0;
       for (uint32_t kb = k0; kb <= k1; kb += 32) {
         const uint32_t k = kb + ln;
         uint32_t v = 0;
         if (k <= k1) {
-          const uint64_t key = (uint64_t)k * kWindow;
+          const uint64_t key = (uint64_t)k * kWinIds;
           v = lb_range(partner + base, 0, len, key < idspace ? (uint32_t)key : idspace);
-          bnd[i * (W + 1) + k] = v;
+          bnd[i * W1 + k] = v;
         }
         uint32_t left = __shfl_up_sync(kFull, v, 1);
         if (ln == 0) left = prev;
-        if (k > k0 && k <= k1 && k - 1 < kWinMaxW && v > left) atomicAdd(&S.ek[k - 1], (unsigned long long)(v - left));
+        if (k > k0 && k <= k1 && v > left) atomicAdd(&S.ek[k - 1 - k0], (unsigned long long)(v - left));
         prev = __shfl_sync(kFull, v, 31);
       }
+    }
+    __syncthreads();
+    for (uint32_t k = k0; k < k1; k++) {
+      uint32_t nch = 0;
+      if (tid < nl) nch = (bnd[tid * W1 + k + 1] - bnd[tid * W1 + k] + kWinChunk - 1) / kWinChunk;
+      uint32_t tot;
+      const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
+      if (tid < nl) cpg[(k - k0) * kWinLists + tid] = cp;
+      if (tid == 0) S.ctot[k - k0] = tot;
     }
   }
   __syncthreads();
   for (uint32_t k = k0; k < k1; k++) {
-    const uint64_t wa = (uint64_t)k * kWindow;
-    const uint64_t wb = wa + kWindow < idspace ? wa + kWindow : idspace;
-    bool dense = pre && k < kWinMaxW && S.ek[k] > kDenseEntries;
-    if (pre && k < kWinMaxW && S.ek[k] == 0) continue;
-    if (!dense) {
+    const uint64_t wa = (uint64_t)k * kWinIds;
+    const uint64_t wb = wa + kWinIds < idspace ? wa + kWinIds : idspace;
+    const uint32_t kr = k - k0;
+    bool dense = pre && S.ek[kr] > kDenseEntries;
+    if (pre && S.ek[kr] == 0) continue;
+    if (!dense && pre && PBNG_WIN_FAST) {
+      // ---- fast path: bitmap + repeat table, chunks statically split over warps
+      if (tid == 0) {
+        sh.over = 0;
+        sh.ndup = 0;
+        sh.next = 0;
+      }
+      const uint32_t tot = S.ctot[kr];
+      const uint32_t* cp = cpg + (uint64_t)kr * kWinLists;
+      for (uint32_t i = tid; i < nl; i += bd) S.cpre[i] = cp[i];
+      __syncthreads();
+      // warps take chunks dynamically; chunk c belongs to the largest list i with cpre[i] <= c
+      auto run = [&](auto&& fn) {
+        for (;;) {
+          uint32_t c = 0;
+          if (ln == 0) c = atomicAdd(&sh.next, 1u);
+          c = __shfl_sync(kFull, c, 0);
+          if (c >= tot) break;
+          uint32_t lo = 0, hi = (uint32_t)nl;
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (S.cpre[mid] <= c) lo = mid; else hi = mid;
+          }
+          const uint64_t sbeg = gbase[lo] + bnd[lo * W1 + k], send = gbase[lo] + bnd[lo * W1 + k + 1];
+          const uint64_t q0 = sbeg + (uint64_t)(c - S.cpre[lo]) * kWinChunk;
+          fn(q0, q0 + kWinChunk < send ? q0 + kWinChunk : send, e0 + lo);
+        }
+      };
+      run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
+      __syncthreads();
+      const bool over = sh.over != 0;
+      const uint32_t nd = min(sh.ndup, kWinDupCap);
+      if (Pass2::kOn && !over && nd) {
+        if (tid == 0) sh.next = 0;
+        __syncthreads();
+        run([&](uint64_t i0, uint64_t i1, uint64_t e) {
+          const unsigned long long cs = win_sum(partner, i0, i1, skip, S);
+          if (ln == 0 && cs) pass2(e, cs);
+        });
+        __syncthreads();
+      }
+      const uint32_t nwords = (uint32_t)((wb - wa + 31) >> 5);
+      for (uint32_t i = tid; i < nwords; i += bd) S.bits[i] = 0;
+      for (uint32_t i = tid; i < nd; i += bd) {
+        const uint32_t sl = S.dslot[i];
+        const unsigned long long v = S.dup[sl];
+        S.dup[sl] = kEmptySlot;
+        if (!over) emit((uint32_t)(v >> 32), (uint32_t)v + 1u);
+      }
+      if (tid == 0) atomicAdd(&dbg[over ? 1 : 0], 1ull);
+      if (over) {
+        for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
+        dense = true;
+      }
+      __syncthreads();
+      if (!dense) continue;
+    } else if (!dense) {
       // bitmap of first occurrences + repeat table over the whole window
       if (tid == 0) {
         sh.over = 0;
@@ -270,15 +424,16 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       }
       __syncthreads();
       auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) { win_mark(partner, i0, i1, (uint32_t)wa, skip, S, sh); };
-      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, wa, wb, partner, S, sh, mark);
+      const uint32_t chunk = kWinChunk;
+      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, wa, wb, partner, S, sh, mark, chunk);
       const bool over = sh.over != 0;
-      const uint32_t nd = min(sh.ndup, kDupCap);
+      const uint32_t nd = min(sh.ndup, kWinDupCap);
       if (Pass2::kOn && any && !over && nd) {
         auto sum = [&](uint64_t i0, uint64_t i1, uint64_t e) {
           const unsigned long long cs = win_sum(partner, i0, i1, skip, S);
           if (ln == 0 && cs) pass2(e, cs);
         };
-        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, wa, wb, partner, S, sh, sum);
+        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, wa, wb, partner, S, sh, sum, chunk);
       }
       if (any) {
         const uint32_t nwords = (uint32_t)((wb - wa + 31) >> 5);
@@ -295,15 +450,21 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         __syncthreads();
         continue;
       }
-      for (uint32_t i = tid; i < kDupSlots; i += bd) S.dup[i] = kEmptySlot;
+      for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
       if (tid == 0) atomicAdd(&dbg[1], 1ull);
       __syncthreads();
     }
     // dense counting in sub-windows of SW ids
     for (uint64_t a = wa; a < wb; a += SW) {
       const uint64_t b = a + SW < wb ? a + SW : wb;
-      auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) { dense_mark(partner, i0, i1, (uint32_t)a, skip, wide, S.bits); };
-      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark);
+      uint32_t* touch = reinterpret_cast<uint32_t*>(S.dup);
+      if (tid == 0) sh.ndup = 0;  // touched-word count
+      __syncthreads();
+      auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) {
+        dense_mark(partner, i0, i1, (uint32_t)a, skip, wide, S.bits, touch, &sh.ndup);
+      };
+      const uint32_t chunk = pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk;
+      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk);
       if (!any) continue;
       if (Pass2::kOn) {
         auto sum = [&](uint64_t i0, uint64_t i1, uint64_t e) {
@@ -315,10 +476,13 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
           cs = warp_sum(cs);
           if (ln == 0 && cs) pass2(e, cs);
         };
-        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum);
+        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum, chunk);
       }
       const uint32_t nwords = wide ? (uint32_t)(b - a) : (uint32_t)((b - a + 1) >> 1);
-      for (uint32_t i = tid; i < nwords; i += bd) {
+      const uint32_t nt = sh.ndup;
+      const bool listed = PBNG_DENSE_TOUCH && nt <= kTouchCap;
+      for (uint32_t t = tid; t < (listed ? nt : nwords); t += bd) {
+        const uint32_t i = listed ? touch[t] : t;
         const uint32_t v = S.bits[i];
         if (v) {
           S.bits[i] = 0;
@@ -334,16 +498,19 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       if (tid == 0) atomicAdd(&dbg[2], 1ull);
       __syncthreads();
     }
+    // the repeat table's memory held touched words: empty it again
+    for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
+    __syncthreads();
   }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kWinThreads, 1) k_agg_win(AggArgs a) {
+__global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
   extern __shared__ __align__(16) unsigned char wsm[];
   WinSmem& S = *reinterpret_cast<WinSmem*>(wsm);
   __shared__ WinShared sh;
-  for (uint32_t i = threadIdx.x; i < kBitWords; i += blockDim.x) S.bits[i] = 0;
-  for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
+  for (uint32_t i = threadIdx.x; i < kWinBitWords; i += blockDim.x) S.bits[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kWinDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
   uint32_t* bnd = a.win_bnd + (uint64_t)blockIdx.x * a.win_cap;
   const uint32_t G = a.win_split;
   const uint64_t n = (uint64_t)*a.count * G;

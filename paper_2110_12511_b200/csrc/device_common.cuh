@@ -215,6 +215,18 @@ __device__ __forceinline__ void cta_wedges(const L& lists, uint64_t e0, uint64_t
   }
 }
 
+// Whole CTA walks all partner lists of one start with the entries flattened
+// over the threads (one list per thread for the length scan, so at most
+// blockDim lists; more fall back to cta_wedges).  Every thread takes entries
+// t, t + blockDim, ... and finds its list by binary search over the scanned
+// lengths, so a start with a few medium lists keeps every warp busy.
+// f(ok, x, e) is called CTA-convergently.  Contains __syncthreads.
+template <class L, class F>
+__device__ __forceinline__ void cta_flat_wedges(const L& lists, uint64_t e0, uint64_t e1,
+                                                const uint32_t* __restrict__ adjV, uint32_t* s_pre,
+                                                unsigned long long* s_base, uint32_t* s_scan, uint32_t* s_long,
+                                                uint32_t* s_nlong, F& f);
+
 // Block-wide exclusive scan of one uint32 per thread (blockDim multiple of 32,
 // <= 1024).  s_warp: 33 uint32 of shared memory.  Returns the exclusive prefix;
 // *total receives the block sum.  Contains __syncthreads.
@@ -244,6 +256,41 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp
   *total = s_warp[32];
   __syncthreads();
   return res;
+}
+
+template <class L, class F>
+__device__ __forceinline__ void cta_flat_wedges(const L& lists, uint64_t e0, uint64_t e1,
+                                                const uint32_t* __restrict__ adjV, uint32_t* s_pre,
+                                                unsigned long long* s_base, uint32_t* s_scan, uint32_t* s_long,
+                                                uint32_t* s_nlong, F& f) {
+  const uint64_t d = e1 - e0;
+  if (d > blockDim.x) {
+    cta_wedges(lists, e0, e1, adjV, s_long, s_nlong, f);
+    return;
+  }
+  uint64_t base = 0;
+  uint32_t len = 0;
+  if (threadIdx.x < d) lists.get(e0 + threadIdx.x, base, len);
+  uint32_t total;
+  const uint32_t pre = block_excl_scan(len, s_scan, &total);
+  if (threadIdx.x < d) {
+    s_pre[threadIdx.x] = pre;
+    s_base[threadIdx.x] = base;
+  }
+  __syncthreads();
+  const uint32_t nd = (uint32_t)d;
+  for (uint32_t t0 = 0; t0 < total; t0 += blockDim.x) {
+    const uint32_t t = t0 + threadIdx.x;
+    const bool ok = t < total;
+    uint32_t lo = 0, hi = nd;  // largest j with s_pre[j] <= t
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t x = ok ? adjV[s_base[lo] + (t - s_pre[lo])] : 0u;
+    f(ok, x, e0 + lo);
+  }
+  __syncthreads();
 }
 
 }  // namespace pbng

@@ -17,21 +17,30 @@ namespace pbng {
 constexpr uint32_t kFdThreads = 512;
 constexpr uint32_t kFdWarpSlots = 512;
 constexpr uint32_t kFdWarpCap = kFdWarpSlots / 2;
+constexpr uint64_t kFdWarpWork = 1u << 15;  // wedges above which a vertex goes to the whole CTA
 
 // ---------------------------------------------------------------- membership
 // A vertex with ⋈^init = 0 is in no butterfly of its partition's subgraph: its
 // tip number is 0 (θ <= support) and peeling it decrements nobody, so it is
 // settled here (θ = 0, peeled) and kept out of the FD member lists.
+// pcount[p]: FD members of p (⋈^init > 0); pall[p]: every vertex of p (the
+// partner ids of a partition's wedges are drawn from these, which bounds the
+// distinct partners of any member)
 __global__ void k_part_count(uint32_t nU, const uint32_t* __restrict__ part, const uint64_t* __restrict__ init,
-                             uint32_t nparts, uint32_t* pcount) {
+                             uint32_t nparts, uint32_t* pcount, uint32_t* pall) {
   extern __shared__ uint32_t hc[];
-  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x) hc[i] = 0;
+  for (uint32_t i = threadIdx.x; i < 2 * nparts; i += blockDim.x) hc[i] = 0;
   __syncthreads();
-  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nU; u += (uint64_t)gridDim.x * blockDim.x)
-    if (init[u]) atomicAdd(&hc[part[u]], 1u);
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nU; u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = part[u];
+    atomicAdd(&hc[nparts + p], 1u);
+    if (init[u]) atomicAdd(&hc[p], 1u);
+  }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x)
+  for (uint32_t i = threadIdx.x; i < nparts; i += blockDim.x) {
     if (hc[i]) atomicAdd(&pcount[i], hc[i]);
+    if (hc[nparts + i]) atomicAdd(&pall[i], hc[nparts + i]);
+  }
 }
 
 // members grouped by partition: members[poff[p] ..) (order inside a group is free)
@@ -129,6 +138,7 @@ struct FdArgs {
   const uint32_t* __restrict__ adjL;
   const uint64_t* __restrict__ seg;
   const uint32_t* __restrict__ poff;
+  const uint32_t* __restrict__ pall;   // vertices per partition (distinct-partner bound)
   const uint32_t* __restrict__ order;  // partition ids, decreasing work (LPT)
   uint32_t nparts;
   uint32_t* ticket;
@@ -190,6 +200,9 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t, s_nbig, s_n0, s_n1;
   __shared__ unsigned long long s_min;
   __shared__ uint32_t s_hist[65];
+  __shared__ uint32_t s_pre[kFdThreads];
+  __shared__ unsigned long long s_base[kFdThreads];
+  __shared__ uint32_t s_scan[33];
   __shared__ FdBand band;
   for (uint32_t i = threadIdx.x; i < nw * 2 * kFdWarpSlots; i += blockDim.x) sm[i] = (i / kFdWarpSlots) % 2 == 0 ? kEmpty : 0u;
   for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) {
@@ -217,6 +230,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
     uint32_t* selpb = a.selpb + lo;
     uint32_t* bigl = a.bigl + lo;
     uint32_t nrest = a.poff[p + 1] - lo;
+    const uint32_t psz = a.pall[p] ? a.pall[p] - 1 : 0;
     uint32_t cb = 0, sb = 0;  // current band / selection buffers
     uint32_t rounds = 0;
     const long long t_start = clock64();
@@ -388,15 +402,19 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         wl = warp_sum(wl);
         if (ln == 0) {
           const uint64_t d = e1 - e0;
-          const uint64_t pb = wl - d;  // u appears once in each of its segments
+          uint64_t pb = wl - d;  // u appears once in each of its segments
           uint32_t r = 0;
           if (d >= 2 && pb > 0 && a.s[u] != 0) {
-            r = pb > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb;
+            if (pb > psz) pb = psz;  // partners are other vertices of this partition
+            r = (uint32_t)pb;
             wedges += wl;
             steps += d;
           }
-          selpb[j] = r;
-          if (r > kFdWarpCap) bigl[atomicAdd(&s_nbig, 1u)] = j;  // whole-CTA work, step (5)
+          // whole-CTA work, step (5): big tables, or long walks a single warp would
+          // serialise (flagged in the top bit)
+          const bool big = r > kFdWarpCap || (r && wl > kFdWarpWork);
+          selpb[j] = big ? (r | 0x80000000u) : r;
+          if (big) bigl[atomicAdd(&s_nbig, 1u)] = j;
         }
       }
       __syncthreads();
@@ -408,7 +426,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       // (4) light: one warp per vertex, per-warp table
       for (uint32_t j = w; j < nsel; j += nw) {
         const uint32_t pb = selpb[j];
-        if (pb == 0 || pb > kFdWarpCap) continue;
+        if (pb == 0 || (pb & 0x80000000u)) continue;
         const uint32_t u = sel[j];
         uint32_t logT = ceil_log2(2 * pb);
         logT = logT < 5 ? 5 : logT;
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
       const uint32_t nbig = s_nbig;
       for (uint32_t bj = 0; bj < nbig; bj++) {
         const uint32_t j = bigl[bj];
-        const uint32_t pb = selpb[j];
+        const uint32_t pb = selpb[j] & 0x7FFFFFFFu;
         const uint32_t u = sel[j];
         if (pb <= kCtaCap) {
           uint32_t logT = ceil_log2(2 * pb);
@@ -446,7 +464,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
           auto f = [&](bool ok, uint32_t x, uint64_t) {
             if (ok && x != u) hash_insert(ckeys, cvals, logT, x);
           };
-          cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_long, &s_nlong, f);
+          cta_flat_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_pre, s_base, s_scan, s_long, &s_nlong, f);
           for (uint32_t s = threadIdx.x; s < (1u << logT); s += blockDim.x) {
             const uint32_t key = ckeys[s];
             if (key != kEmpty) {
@@ -487,7 +505,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
               if (second) hdup[base + __popc(m & lanemask_lt())] = x;
             }
           };
-          cta_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_long, &s_nlong, f);
+          cta_flat_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_pre, s_base, s_scan, s_long, &s_nlong, f);
           const uint32_t nd = s_ndup, nt = s_ntouch;
           for (uint32_t q = threadIdx.x; q < nd; q += blockDim.x) {
             const uint32_t key = hdup[q];

@@ -382,12 +382,12 @@ __global__ void __launch_bounds__(kMidThreads, 1) k_vp_agg_mid(AggArgs a) {
 
 // Tier 2: one CTA per start, window bitmap over segments (agg_win.cuh).
 template <int SIDE>
-__global__ void __launch_bounds__(kWinThreads, 1) k_vp_agg_win(AggArgs a) {
+__global__ void __launch_bounds__(kWinThreads, kWinCtas) k_vp_agg_win(AggArgs a) {
   extern __shared__ __align__(16) unsigned char wsm[];
   WinSmem& S = *reinterpret_cast<WinSmem*>(wsm);
   __shared__ WinShared sh;
-  for (uint32_t i = threadIdx.x; i < kBitWords; i += blockDim.x) S.bits[i] = 0;
-  for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
+  for (uint32_t i = threadIdx.x; i < kWinBitWords; i += blockDim.x) S.bits[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kWinDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
   uint32_t* bnd = a.win_bnd + (uint64_t)blockIdx.x * a.win_cap;
   const uint32_t G = a.win_split;
   const uint64_t n = (uint64_t)*a.count * G;

@@ -467,9 +467,9 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank&
   S.piece_head = r.alloc<uint32_t>(np);
   S.piece_srange = r.alloc<uint32_t>(np);
   S.piece_pedge = vp ? r.alloc<uint64_t>(np) : nullptr;
-  const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWindow - 1) / kWindow;
-  S.win_cap = (uint64_t)kWinLists * (wmax + 1);
-  S.win_bnd = r.alloc<uint32_t>((size_t)r.nsm * S.win_cap);
+  const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWinIds - 1) / kWinIds;
+  S.win_cap = 2 * (uint64_t)kWinLists * (wmax + 1) + 2 * (uint64_t)kWinLists;  // bounds, chunk prefixes, bases
+  S.win_bnd = r.alloc<uint32_t>((size_t)r.nsm * kWinCtas * S.win_cap);
 }
 
 AggArgs agg_args(const State& S, int t) {
@@ -502,18 +502,23 @@ AggArgs agg_args(const State& S, int t) {
 }
 
 template <int MODE>
-void launch_agg(Run& r, const State& S) {
-  r.pre(PBNG_K_AGG_WARP);
-  k_agg_warp<MODE><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
-  r.post(PBNG_K_AGG_WARP);
-  r.pre(PBNG_K_AGG_CTA);
-  r.post(PBNG_K_AGG_CTA);
-  r.pre(PBNG_K_AGG_CTA);
-  k_agg_mid<MODE><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
-  r.post(PBNG_K_AGG_CTA);
-  r.pre(PBNG_K_AGG_CTA);
-  k_agg_win<MODE><<<r.nsm, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
-  r.post(PBNG_K_AGG_CTA);
+void launch_agg(Run& r, const State& S, const uint32_t* ntier) {
+  // ntier: tier sizes read back by the host (launch only non-empty tiers)
+  if (ntier[0]) {
+    r.pre(PBNG_K_AGG_WARP);
+    k_agg_warp<MODE><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
+    r.post(PBNG_K_AGG_WARP);
+  }
+  if (ntier[1]) {
+    r.pre(PBNG_K_AGG_CTA);
+    k_agg_mid<MODE><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+    r.post(PBNG_K_AGG_CTA);
+  }
+  if (ntier[2]) {
+    r.pre(PBNG_K_AGG_CTA);
+    k_agg_win<MODE><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
+    r.post(PBNG_K_AGG_CTA);
+  }
 }
 
 void reset_tiers(Run& r, State& S) {
@@ -523,9 +528,9 @@ void reset_tiers(Run& r, State& S) {
 // Tier-2 starts are split into window groups when a batch has fewer than two
 // starts per SM, so that small batches still occupy every SM.
 uint32_t pick_split(const Run& r, uint32_t n2, uint32_t idspace) {
-  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWindow - 1) / kWindow);
+  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
   if (n2 == 0 || W <= 1) return 1;
-  const uint32_t want = (2u * (uint32_t)r.nsm + n2 - 1) / n2;
+  const uint32_t want = (2u * (uint32_t)r.nsm * kWinCtas + n2 - 1) / n2;
   return std::max(1u, std::min(want, W));
 }
 
@@ -550,7 +555,7 @@ void vp_count_live(Run& r, State& S) {
   k_vp_agg_mid<0><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
   r.post(PBNG_K_AGG_CTA);
   r.pre(PBNG_K_AGG_CTA);
-  k_vp_agg_win<0><<<r.nsm, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
+  k_vp_agg_win<0><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
   r.post(PBNG_K_AGG_CTA);
   // starts in V
   reset_tiers(r, S);
@@ -565,7 +570,7 @@ void vp_count_live(Run& r, State& S) {
   k_vp_agg_mid<1><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
   r.post(PBNG_K_AGG_CTA);
   r.pre(PBNG_K_AGG_CTA);
-  k_vp_agg_win<1><<<r.nsm, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
+  k_vp_agg_win<1><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
   r.post(PBNG_K_AGG_CTA);
 }
 
@@ -586,8 +591,9 @@ void count_live(Run& r, State& S) {
   k_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, S.g.offU, S.g.adjU, S.ld, S.support, S.tier[0],
                                                   S.tier[1], S.tier[2], nullptr, 0, S.c);
   r.post(PBNG_K_CLASSIFY);
-  S.win_split = pick_split(r, r.readback(S.c).ntier[2], S.g.nU);
-  launch_agg<0>(r, S);
+  const Counters hc = r.readback(S.c);
+  S.win_split = pick_split(r, hc.ntier[2], S.g.nU);
+  launch_agg<0>(r, S, hc.ntier);
 }
 
 void compact(Run& r, State& S, uint32_t epoch) {
@@ -629,7 +635,7 @@ struct Plan {
 // Coarse-grained decomposition (Alg.4 structure P:799-816, tip P:982-991).
 struct TraceRow {
   uint32_t pid, nF, t0, t1, t2;
-  unsigned long long wedges;
+  unsigned long long wedges, w2cum;  // batch wedges; cumulative tier-2 wedges after classify
   bool recount;
   cudaEvent_t a, b;
 };
@@ -726,11 +732,12 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         st.recounts++;
       } else {
         S.win_split = pick_split(r, hc.ntier[2], nU);
-        launch_agg<1>(r, S);
+        launch_agg<1>(r, S, hc.ntier);
         if (del) compact(r, S, epoch);
       }
       if (trace) {
-        TraceRow row{pid, hc.nF, hc.ntier[0], hc.ntier[1], hc.ntier[2], hc.wedges, recount, ta, r.event()};
+        TraceRow row{pid, hc.nF, hc.ntier[0], hc.ntier[1], hc.ntier[2], hc.wedges, hc.tier_wedges[2], recount, ta,
+                     r.event()};
         rows.push_back(row);
       }
     }
@@ -742,8 +749,8 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
   if (trace) {
     CK(cudaStreamSynchronize(r.st));
     for (const TraceRow& t : rows)
-      std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu recount=%d ms=%.3f\n", t.pid, t.nF, t.t0,
-                   t.t1, t.t2, t.wedges, (int)t.recount, elapsed(t.a, t.b));
+      std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu w2cum=%llu recount=%d ms=%.3f\n", t.pid,
+                   t.nF, t.t0, t.t1, t.t2, t.wedges, t.w2cum, (int)t.recount, elapsed(t.a, t.b));
   }
 }
 
@@ -751,7 +758,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
 void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st, float& ms_build) {
   const uint32_t np = plan.nparts, nU = S.g.nU;
   cudaEvent_t e0 = r.event();
-  uint32_t* pcount = r.alloc<uint32_t>(np);
+  uint32_t* pcount = r.alloc<uint32_t>(2 * np);  // [0, np) FD members, [np, 2np) all vertices
   uint32_t* poff = r.alloc<uint32_t>(np + 1);
   uint32_t* pcur = r.alloc<uint32_t>(np);
   unsigned long long* work = r.alloc<unsigned long long>(np);
@@ -767,14 +774,14 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   uint64_t* seg = r.alloc<uint64_t>(S.g.m);
   unsigned long long* fdc = r.alloc<unsigned long long>(3);  // wedges, updates, steps
   uint32_t* misc = r.alloc<uint32_t>(3);                     // ticket, rounds_max, heavy count
-  CK(cudaMemsetAsync(pcount, 0, (size_t)np * 4, r.st));
+  CK(cudaMemsetAsync(pcount, 0, (size_t)np * 8, r.st));
   CK(cudaMemsetAsync(pcur, 0, (size_t)np * 4, r.st));
   CK(cudaMemsetAsync(work, 0, (size_t)np * 8, r.st));
   CK(cudaMemsetAsync(fstate, 0, (size_t)nU * 4, r.st));
   CK(cudaMemsetAsync(fdc, 0, 24, r.st));
   CK(cudaMemsetAsync(misc, 0, 12, r.st));
   r.pre(PBNG_K_FD_BUILD);
-  k_part_count<<<r.nsm * 4, 256, np * 4, r.st>>>(nU, S.part, S.init, np, pcount);
+  k_part_count<<<r.nsm * 4, 256, np * 8, r.st>>>(nU, S.part, S.init, np, pcount, pcount + np);
   r.post(PBNG_K_FD_BUILD);
   std::vector<uint32_t> hcount(np), hoff(np + 1);
   CK(cudaMemcpyAsync(hcount.data(), pcount, (size_t)np * 4, cudaMemcpyDeviceToHost, r.st));
@@ -816,6 +823,7 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   a.adjL = S.adjL;
   a.seg = seg;
   a.poff = poff;
+  a.pall = pcount + np;
   a.order = order;
   a.nparts = np;
   a.ticket = misc;
