@@ -252,8 +252,10 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
   return any;
 }
 
-// Dense sub-window: 16-bit counters (two per word) over kDenseIds ids, or
-// 32-bit counters over kDenseIds / 2 ids when a start has >= 2^16 lists
+// Dense sub-window: counters of `lb` = log2(bits) packed 32/bits per word; the
+// field width is the smallest of 2, 4, 8, 16, 32 bits that holds the number of
+// lists of the start (w counts lists, each list holds an id at most once), so a
+// start with few lists counts 256K or 512K ids per pass over the 128 KB array
 // (w <= number of lists).
 constexpr uint32_t kDenseIds = kWinBitWords * 2;
 constexpr uint64_t kDenseEntries = 1u << 16;  // coarse windows with more entries go dense
@@ -263,17 +265,22 @@ constexpr uint32_t kWinMaxW = 64;              // windows whose entry counts are
 // appends the word to the touched list (kept in the repeat table's memory,
 // which dense mode does not use), so the sweep visits touched words only.
 constexpr uint32_t kTouchCap = kWinDupSlots * 2;
+__device__ __forceinline__ uint32_t dense_log_bits(uint64_t nl) {
+  return nl < 4 ? 1u : nl < 16 ? 2u : nl < 256 ? 3u : nl < 65536 ? 4u : 5u;  // log2 of 2..32 bits
+}
+
 __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
-                                           uint32_t skip, bool wide, uint32_t* cnt, uint32_t* touch,
+                                           uint32_t skip, uint32_t lb, uint32_t* cnt, uint32_t* touch,
                                            uint32_t* ntouch) {
   const uint32_t ln = lane_id();
+  const uint32_t lf = 5 - lb;  // log2 fields per word
   auto one = [&](bool ok, uint32_t x) {
     bool fresh = false;
     uint32_t wd = 0;
     if (ok && x != skip) {
       const uint32_t o = x - a;
-      wd = wide ? o : o >> 1;
-      fresh = atomicAdd(&cnt[wd], wide ? 1u : 1u << ((o & 1) << 4)) == 0u;
+      wd = o >> lf;
+      fresh = atomicAdd(&cnt[wd], 1u << ((o & ((1u << lf) - 1)) << lb)) == 0u;
     }
     const uint32_t m = __ballot_sync(kFull, fresh);
     if (m) {
@@ -287,8 +294,10 @@ __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint6
   };
   seg_visit(p, i0, i1, one);
 }
-__device__ __forceinline__ uint32_t dense_get(const uint32_t* cnt, uint32_t o, bool wide) {
-  return wide ? cnt[o] : (cnt[o >> 1] >> ((o & 1) << 4)) & 0xFFFFu;
+__device__ __forceinline__ uint32_t dense_get(const uint32_t* cnt, uint32_t o, uint32_t lb) {
+  const uint32_t lf = 5 - lb, bits = 1u << lb;
+  const uint32_t v = cnt[o >> lf] >> ((o & ((1u << lf) - 1)) << lb);
+  return bits == 32 ? v : v & ((1u << bits) - 1);
 }
 
 // Aggregate w(start, x) over all wedges of one start (lists e in [e0, e1),
@@ -314,8 +323,8 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   // fast path: every list's window bounds, base and per-window chunk prefixes
   // are computed once per start (per-CTA scratch), so a window needs no scan
   const bool pre = nl <= kWinLists && k1 - k0 <= kWinMaxW;
-  const bool wide = nl >= 0xFFFFull;
-  const uint32_t SW = wide ? kDenseIds / 2 : kDenseIds;
+  const uint32_t lb = dense_log_bits(nl);                 // dense counter width 2^lb bits
+  const uint32_t SW = kWinBitWords << (5 - lb);           // ids per dense pass
   const uint32_t W1 = W + 1;
   uint32_t* cpg = bnd + (uint64_t)kWinLists * W1;                        // [kr * kWinLists + i]
   unsigned long long* gbase = reinterpret_cast<unsigned long long*>(cpg + (uint64_t)kWinLists * W1);
@@ -461,7 +470,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       if (tid == 0) sh.ndup = 0;  // touched-word count
       __syncthreads();
       auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) {
-        dense_mark(partner, i0, i1, (uint32_t)a, skip, wide, S.bits, touch, &sh.ndup);
+        dense_mark(partner, i0, i1, (uint32_t)a, skip, lb, S.bits, touch, &sh.ndup);
       };
       const uint32_t chunk = pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk;
       const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk);
@@ -471,14 +480,15 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
           unsigned long long cs = 0;
           for (uint64_t q = i0 + ln; q < i1; q += 32) {
             const uint32_t x = partner[q];
-            if (x != skip) cs += dense_get(S.bits, x - (uint32_t)a, wide) - 1u;
+            if (x != skip) cs += dense_get(S.bits, x - (uint32_t)a, lb) - 1u;
           }
           cs = warp_sum(cs);
           if (ln == 0 && cs) pass2(e, cs);
         };
         win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum, chunk);
       }
-      const uint32_t nwords = wide ? (uint32_t)(b - a) : (uint32_t)((b - a + 1) >> 1);
+      const uint32_t fpw = 1u << (5 - lb);  // fields per word
+      const uint32_t nwords = (uint32_t)((b - a + fpw - 1) / fpw);
       const uint32_t nt = sh.ndup;
       const bool listed = PBNG_DENSE_TOUCH && nt <= kTouchCap;
       for (uint32_t t = tid; t < (listed ? nt : nwords); t += bd) {
@@ -486,12 +496,11 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         const uint32_t v = S.bits[i];
         if (v) {
           S.bits[i] = 0;
-          if (wide) {
-            if (v >= 2) emit((uint32_t)a + i, v);
-          } else {
-            const uint32_t lo = v & 0xFFFFu, hi = v >> 16;
-            if (lo >= 2) emit((uint32_t)a + 2 * i, lo);
-            if (hi >= 2) emit((uint32_t)a + 2 * i + 1, hi);
+          const uint32_t bits = 1u << lb;
+          const uint32_t mask = bits == 32 ? 0xFFFFFFFFu : (1u << bits) - 1;
+          for (uint32_t f = 0; f < fpw; f++) {
+            const uint32_t c = (v >> (f << lb)) & mask;
+            if (c >= 2) emit((uint32_t)a + i * fpw + f, c);
           }
         }
       }
