@@ -12,26 +12,44 @@ constexpr uint32_t kMidThreads = 512;
 struct MidSmem {
   uint32_t keys[kCtaSlots];
   uint32_t vals[kCtaSlots];
+  uint16_t used[kCtaCap];               // slots taken, in insertion order (sweep list)
   uint32_t s_long[kMidThreads];
+  uint32_t s_pre[kMidThreads];
+  unsigned long long s_base[kMidThreads];
+  uint32_t s_scan[33];
+  uint32_t nused;
 };
 
 // Aggregate w over the wedges of one start (lists e in [e0, e1)), keeping
 // partners x with keep(x); then, if pass2 is on, walk the wedges again and
-// call pass2_list(e, Σ (w - 1)) per list; finally emit(k, w) for every partner.
-// Call with the whole CTA; the table is empty on entry and on exit.
+// call pass2(e, Σ (w - 1)) per list; finally emit(k, w) for every partner.
+// The walk flattens the start's entries over the whole CTA; the sweep visits
+// only the slots taken.  Call with the whole CTA; the table is empty on entry
+// and on exit.
 template <class L, class Keep, class Emit, class Pass2 = NoPass2>
 __device__ __forceinline__ void mid_agg_one(const L& lists, uint64_t e0, uint64_t e1,
                                             const uint32_t* __restrict__ partner, uint32_t pb, MidSmem& S,
                                             uint32_t* s_nlong, const Keep& keep, Emit& emit,
                                             const Pass2& pass2 = Pass2()) {
+  const uint32_t ln = lane_id();
   uint32_t logT = ceil_log2(2 * pb);
   logT = logT < 5 ? 5 : (logT > kLogCtaSlots ? kLogCtaSlots : logT);
+  if (threadIdx.x == 0) S.nused = 0;
+  __syncthreads();
   auto f = [&](bool ok, uint32_t x, uint64_t) {
-    if (ok && keep(x)) hash_insert(S.keys, S.vals, logT, x);
+    const uint32_t sl = ok && keep(x) ? hash_insert_new(S.keys, S.vals, logT, x) : 0xFFFFFFFFu;
+    const bool fresh = sl != 0xFFFFFFFFu;
+    const uint32_t m = __ballot_sync(kFull, fresh);
+    if (m) {
+      const uint32_t leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (ln == leader) base = atomicAdd(&S.nused, (uint32_t)__popc(m));
+      base = __shfl_sync(kFull, base, leader);
+      if (fresh) S.used[base + __popc(m & lanemask_lt())] = (uint16_t)sl;
+    }
   };
-  cta_wedges(lists, e0, e1, partner, S.s_long, s_nlong, f);
+  cta_flat_wedges(lists, e0, e1, partner, S.s_pre, S.s_base, S.s_scan, S.s_long, s_nlong, f);
   if (Pass2::kOn) {
-    const uint32_t ln = lane_id();
     auto f2 = [&](bool ok, uint32_t x, uint64_t e) {
       unsigned long long val = 0;
       if (ok && keep(x)) val = hash_lookup(S.keys, S.vals, logT, x) - 1u;
@@ -45,17 +63,16 @@ __device__ __forceinline__ void mid_agg_one(const L& lists, uint64_t e0, uint64_
       const uint64_t kn = __shfl_down_sync(kFull, key, 1);
       if (ok && (ln == 31 || kn != key) && val) pass2(e, val);
     };
-    cta_wedges(lists, e0, e1, partner, S.s_long, s_nlong, f2);
+    cta_flat_wedges(lists, e0, e1, partner, S.s_pre, S.s_base, S.s_scan, S.s_long, s_nlong, f2);
   }
-  const uint32_t T = 1u << logT;
-  for (uint32_t s = threadIdx.x; s < T; s += blockDim.x) {
+  const uint32_t nu = S.nused;
+  for (uint32_t i = threadIdx.x; i < nu; i += blockDim.x) {
+    const uint32_t s = S.used[i];
     const uint32_t k = S.keys[s];
-    if (k != kEmpty) {
-      const uint32_t w = S.vals[s];
-      S.keys[s] = kEmpty;
-      S.vals[s] = 0;
-      emit(k, w);
-    }
+    const uint32_t w = S.vals[s];
+    S.keys[s] = kEmpty;
+    S.vals[s] = 0;
+    emit(k, w);
   }
   __syncthreads();
 }

@@ -127,7 +127,7 @@ struct VpSide<1> {  // start ∈ V
 // tier 1 (CTA).  A warp takes 32 starts and walks their edges flattened.
 template <int SIDE>
 __global__ void __launch_bounds__(256) k_vp_classify(uint32_t n, AggArgs a, uint2* tier0, uint2* tier1,
-                                                     uint2* tier2) {
+                                                     uint2* tier2, uint2* bigq) {
   __shared__ unsigned long long s_acc[8][32];
   const uint32_t ln = lane_id();
   unsigned long long* acc = s_acc[threadIdx.x >> 5];
@@ -142,6 +142,13 @@ __global__ void __launch_bounds__(256) k_vp_classify(uint32_t n, AggArgs a, uint
     if (SIDE == 0 && ok && a.part[x] != kUnassigned) ok = false;
     uint64_t e0 = 0, e1 = 0;
     if (ok) VpSide<SIDE>::range(a, x, e0, e1);
+    // hub starts are summed by a whole CTA (k_vp_classify_big)
+    const bool big = e1 - e0 > kClassBig;
+    warp_append2(big, make_uint2(x, 0), bigq, &a.c->nbig);
+    if (big) {
+      ok = false;
+      e1 = e0;
+    }
     const uint64_t d = e1 - e0;
     uint64_t incl = d;
 #pragma unroll
@@ -202,6 +209,44 @@ __global__ void __launch_bounds__(256) k_vp_classify(uint32_t n, AggArgs a, uint
     atomicAdd(&a.c->wedges, wsum);
     atomicAdd(&a.c->cum_wedges, wsum);
     atomicAdd(&a.c->cum_steps, ssum);
+  }
+}
+
+// The starts k_vp_classify deferred (more than kClassBig lists): one CTA each.
+template <int SIDE>
+__global__ void __launch_bounds__(512) k_vp_classify_big(AggArgs a, const uint2* __restrict__ bigq, uint2* tier0,
+                                                         uint2* tier1, uint2* tier2) {
+  __shared__ unsigned long long s_part[16];
+  const uint32_t n = a.c->nbig;
+  const auto L = VpSide<SIDE>::lists(a);
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t x = bigq[i].x;
+    uint64_t e0, e1;
+    VpSide<SIDE>::range(a, x, e0, e1);
+    unsigned long long s = 0;
+    for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      uint64_t base;
+      uint32_t len;
+      L.get(e, base, len);
+      s += len;
+    }
+    s = warp_sum(s);
+    if (lane_id() == 0) s_part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); w++) s += s_part[w];
+      if (s) {
+        const uint32_t pb = s > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)s;
+        const int tier = pb <= kWarpCap ? 0 : pb <= kCtaCap ? 1 : 2;
+        uint2* tl = tier == 0 ? tier0 : tier == 1 ? tier1 : tier2;
+        tl[atomicAdd(&a.c->ntier[tier], 1u)] = make_uint2(x, pb);
+        atomicAdd(&a.c->wedges, s);
+        atomicAdd(&a.c->cum_wedges, s);
+        atomicAdd(&a.c->cum_steps, (unsigned long long)(e1 - e0));
+      }
+    }
+    __syncthreads();
   }
 }
 

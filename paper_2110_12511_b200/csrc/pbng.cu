@@ -545,7 +545,10 @@ void vp_count_live(Run& r, State& S) {
   // starts in U
   reset_tiers(r, S);
   r.pre(PBNG_K_CLASSIFY);
-  k_vp_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(g.nU, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2]);
+  k_vp_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(g.nU, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2], S.tier[3]);
+  r.post(PBNG_K_CLASSIFY);
+  r.pre(PBNG_K_CLASSIFY);
+  k_vp_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(agg_args(S, 0), S.tier[3], S.tier[0], S.tier[1], S.tier[2]);
   r.post(PBNG_K_CLASSIFY);
   S.win_split = pick_split(r, r.readback(S.c).ntier[2], g.nU);
   r.pre(PBNG_K_AGG_WARP);
@@ -560,7 +563,10 @@ void vp_count_live(Run& r, State& S) {
   // starts in V
   reset_tiers(r, S);
   r.pre(PBNG_K_CLASSIFY);
-  k_vp_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(g.nV, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2]);
+  k_vp_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(g.nV, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2], S.tier[3]);
+  r.post(PBNG_K_CLASSIFY);
+  r.pre(PBNG_K_CLASSIFY);
+  k_vp_classify_big<1><<<r.nsm * 2, 512, 0, r.st>>>(agg_args(S, 0), S.tier[3], S.tier[0], S.tier[1], S.tier[2]);
   r.post(PBNG_K_CLASSIFY);
   S.win_split = pick_split(r, r.readback(S.c).ntier[2], g.nV);
   r.pre(PBNG_K_AGG_WARP);
