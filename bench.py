@@ -163,6 +163,21 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------- replicas (N > 1)
+def max_over_ranks(ms: float, dist=None, device="cpu") -> float:
+    """Device-measured time of this rank -> max over all ranks (the job's time)."""
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_rate(units_per_rank: float, world: int, max_ms: float) -> float:
+    """Whole-job throughput: the units every rank processed / the slowest rank's time."""
+    return world * units_per_rank / (max_ms / 1000.0)
+
+
 # ---------------------------------------------------------------- GPU arm
 def roofline(stats_list, peaks):
     """Dominant kernel family: the wedge aggregation (k_agg_warp/cta/heavy tiers)."""
@@ -237,11 +252,8 @@ def run_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
     wedges_step = stats[-1]["wedges_count"] + stats[-1]["wedges_cd"] + stats[-1]["wedges_fd"]
-    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    value = world * wedges_step * args.steps / (max_ms / 1000)
+    max_ms = max_over_ranks(total_ms, dist, device=f"cuda:{local}")
+    value = job_rate(wedges_step * args.steps, world, max_ms)
     # ---- end to end through the host-buffer C ABI entry point (pinned host CSR in, θ out)
     e2e = None
     if not args.no_e2e:
@@ -264,13 +276,11 @@ def run_gpu(args):
             e1.record(stream)
             e1.synchronize()
             e2e_ms += e0.elapsed_time(e1)
-        t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-        if dist:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * wedges_step * args.steps / (float(t2.item()) / 1000), "unit": UNIT,
+        e2e_max = max_over_ranks(e2e_ms, dist, device=f"cuda:{local}")
+        e2e = {"value": job_rate(wedges_step * args.steps, world, e2e_max), "unit": UNIT,
                "h2d_bytes_per_step": int(sum(p.numel() * p.element_size() for p in pin)),
                "d2h_bytes_per_step": int(g.nU * 8),
-               "seconds_per_decomposition": float(t2.item()) / 1000 / args.steps,
+               "seconds_per_decomposition": e2e_max / 1000 / args.steps,
                "api": "pbng_tip_decompose_host (C ABI, pinned host buffers)"}
     if rank != 0:
         if dist:
@@ -309,6 +319,36 @@ def run_gpu(args):
     return 0
 
 
+def run_ablation(args):
+    """Paper §5 optimisations on the workload (shape of fig:optTip):
+    PBNG (all), PBNG- (no dynamic deletion), PBNG-- (no deletion, no batch re-count),
+    and one-sided instead of vertex-priority counting; both peel sides.  One JSON
+    line per variant (not the driver's metric line)."""
+    import torch
+    locked_build()
+    import paper_2110_12511_b200 as pb
+    g, P, _ = load_graph(args.config)
+    variants = [("PBNG", 0), ("PBNG-", pb.OPT_NO_DELETE), ("PBNG--", pb.OPT_NO_DELETE | pb.OPT_NO_RECOUNT),
+                ("PBNG+onesided-count", pb.OPT_ONESIDED_COUNT)]
+    d = pb.DeviceGraph.from_numpy(g.off_u, g.adj_u, g.off_v, g.adj_v)
+    for side in (0, 1):
+        for name, opts in variants:
+            pb.pbng_tip_decompose(d, P, side=side, opts=opts | pb.OPT_STATS)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, st = pb.pbng_tip_decompose(d, P, side=side, opts=opts | pb.OPT_STATS)
+            e1.record()
+            e1.synchronize()
+            w = st["wedges_count"] + st["wedges_cd"] + st["wedges_fd"]
+            print(json.dumps({"ablation": name, "config": workload_desc(args.config, g, P), "side": side,
+                              "seconds": e0.elapsed_time(e1) / 1000, "wedges": w,
+                              "wedges_count": st["wedges_count"], "wedges_cd": st["wedges_cd"],
+                              "wedges_fd": st["wedges_fd"], "rho_cd_iters": st["rho_cd_iters"],
+                              "recounts": st["recounts"]}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -319,7 +359,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-wedges", type=float, default=5e8, help="oracle wedges per reference step")
+    ap.add_argument("--ablation", action="store_true", help="PBNG / PBNG- / PBNG-- / one-sided count, both sides")
     args = ap.parse_args()
+    if args.ablation:
+        return run_ablation(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

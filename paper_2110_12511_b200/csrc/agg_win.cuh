@@ -258,7 +258,10 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
 // start with few lists counts 256K or 512K ids per pass over the 128 KB array
 // (w <= number of lists).
 constexpr uint32_t kDenseIds = kWinBitWords * 2;
-constexpr uint64_t kDenseEntries = 1u << 16;  // coarse windows with more entries go dense
+#ifndef PBNG_DENSE_ENTRIES
+#define PBNG_DENSE_ENTRIES 65536
+#endif
+constexpr uint64_t kDenseEntries = PBNG_DENSE_ENTRIES;  // coarse windows with more entries go dense
 constexpr uint32_t kWinMaxW = 64;              // windows whose entry counts are kept in shared memory
 
 // Dense marking: one atomicAdd per wedge; the first increment of a word
@@ -328,6 +331,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   const uint32_t W1 = W + 1;
   uint32_t* cpg = bnd + (uint64_t)kWinLists * W1;                        // [kr * kWinLists + i]
   unsigned long long* gbase = reinterpret_cast<unsigned long long*>(cpg + (uint64_t)kWinLists * W1);
+  const long long tp0 = clock64();
   for (uint32_t k = tid; k < kWinMaxW; k += bd) S.ek[k] = 0;
   __syncthreads();
   if (pre) {
@@ -363,6 +367,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     }
   }
   __syncthreads();
+  if (tid == 0) atomicAdd(&dbg[5], (unsigned long long)(clock64() - tp0));
   for (uint32_t k = k0; k < k1; k++) {
     const uint64_t wa = (uint64_t)k * kWinIds;
     const uint64_t wb = wa + kWinIds < idspace ? wa + kWinIds : idspace;
@@ -397,8 +402,11 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
           fn(q0, q0 + kWinChunk < send ? q0 + kWinChunk : send, e0 + lo);
         }
       };
+      const long long tm0 = clock64();
       run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       __syncthreads();
+      const long long tm1 = clock64();
+      if (tid == 0) atomicAdd(&dbg[6], (unsigned long long)(tm1 - tm0));
       const bool over = sh.over != 0;
       const uint32_t nd = min(sh.ndup, kWinDupCap);
       if (Pass2::kOn && !over && nd) {
@@ -419,6 +427,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         if (!over) emit((uint32_t)(v >> 32), (uint32_t)v + 1u);
       }
       if (tid == 0) atomicAdd(&dbg[over ? 1 : 0], 1ull);
+      if (tid == 0) atomicAdd(&dbg[7], (unsigned long long)(clock64() - tm1));
       if (over) {
         for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
         dense = true;
@@ -536,7 +545,9 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     const uint32_t u = a.list[t / G].x;
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
+    const long long ts0 = clock64();
     win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, out, a.c->dbg);
+    if (threadIdx.x == 0) atomicAdd(&a.c->prof[0], (unsigned long long)(clock64() - ts0));
     if (MODE == 0) {
       acc = warp_sum(acc);
       if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);

@@ -76,6 +76,22 @@ __device__ __forceinline__ void hash_insert(uint32_t* keys, uint32_t* vals, uint
   atomicAdd(&vals[h], 1u);
 }
 
+// Add c occurrences of k (open addressing as hash_insert).
+__device__ __forceinline__ void hash_add(uint32_t* keys, uint32_t* vals, uint32_t logT, uint32_t k, uint32_t c) {
+  const uint32_t mask = (1u << logT) - 1;
+  uint32_t h = (k * 0x9E3779B1u) >> (32 - logT);
+  for (;;) {
+    uint32_t cur = ((volatile uint32_t*)keys)[h];
+    if (cur == k) break;
+    if (cur == kEmpty) {
+      cur = atomicCAS(&keys[h], kEmpty, k);
+      if (cur == kEmpty || cur == k) break;
+    }
+    h = (h + 1) & mask;
+  }
+  atomicAdd(&vals[h], c);
+}
+
 // hash_insert that also reports the slot when k was new (else 0xFFFFFFFF).
 __device__ __forceinline__ uint32_t hash_insert_new(uint32_t* keys, uint32_t* vals, uint32_t logT, uint32_t k) {
   const uint32_t mask = (1u << logT) - 1;

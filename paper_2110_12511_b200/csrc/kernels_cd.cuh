@@ -79,7 +79,8 @@ struct Counters {
   unsigned long long cum_wedges; // Σ of every classify's wedges
   unsigned long long cum_steps;  // Σ d_u of every traversed u ((u, v) steps)
   unsigned long long tier_wedges[3];  // Σ wl routed to each tier
-  unsigned long long dbg[4];          // tier-1 internals: ranges, replays, steps, pieces walked
+  unsigned long long dbg[4];          // tier-2 internals: bitmap windows, overflows, dense passes, -
+  unsigned long long prof[4];         // tier-2 clock64 of CTA thread 0: whole starts, precompute, marking, after-marking
 };
 
 // ---------------------------------------------------------------- init
@@ -324,7 +325,10 @@ struct AggArgs {
 
 template <int MODE>
 __device__ __forceinline__ void emit(const AggArgs& a, uint32_t k, uint32_t w, uint64_t& acc, unsigned long long& upd) {
-  if (w >= 2 && a.part[k] == kUnassigned) {
+  // PEEL skips the liveness test: a peeled partner's support is never read again
+  // (selection, snapshots and FD only read live vertices), so decrementing it is
+  // harmless and saves a random load per emitted pair
+  if (w >= 2 && (MODE == 1 || a.part[k] == kUnassigned)) {
     const uint64_t d = choose2(w);
     if (MODE == 0) {
       acc += d;

@@ -458,7 +458,37 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
         const uint32_t j = bigl[bj];
         const uint32_t pb = selpb[j] & 0x7FFFFFFFu;
         const uint32_t u = sel[j];
-        if (pb <= kCtaCap) {
+        if (pb <= kFdWarpCap) {
+          // few distinct partners but a long walk: every warp counts its share of
+          // the entries in its own table (no cross-warp contention on hot keys),
+          // then the warp tables are summed into the CTA table
+          uint32_t logT = ceil_log2(2 * pb);
+          logT = logT < 5 ? 5 : logT;
+          auto f = [&](bool ok, uint32_t x, uint64_t) {
+            if (ok && x != u) hash_insert(wkeys, wvals, logT, x);
+          };
+          cta_flat_wedges(L, a.offU[u], a.offU[u + 1], a.adjL, s_pre, s_base, s_scan, s_long, &s_nlong, f);
+          for (uint32_t s = ln; s < (1u << logT); s += 32) {
+            const uint32_t key = wkeys[s];
+            if (key != kEmpty) {
+              const uint32_t c = wvals[s];
+              wkeys[s] = kEmpty;
+              wvals[s] = 0;
+              hash_add(ckeys, cvals, logT, key, c);
+            }
+          }
+          __syncthreads();
+          for (uint32_t s = threadIdx.x; s < (1u << logT); s += blockDim.x) {
+            const uint32_t key = ckeys[s];
+            if (key != kEmpty) {
+              const uint32_t wv = cvals[s];
+              ckeys[s] = kEmpty;
+              cvals[s] = 0;
+              fd_emit(a, key, wv, upd, band);
+            }
+          }
+          __syncthreads();
+        } else if (pb <= kCtaCap) {
           uint32_t logT = ceil_log2(2 * pb);
           logT = logT > 14 ? 14 : logT;
           auto f = [&](bool ok, uint32_t x, uint64_t) {

@@ -753,7 +753,9 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
   plan.nparts = (uint32_t)plan.bounds.size() - 1;
   if (plan.nparts) plan.bounds.back() = kInf;
   if (trace) {
-    CK(cudaStreamSynchronize(r.st));
+    const Counters hc = r.readback(S.c);
+    std::fprintf(stderr, "tier2 cycles: starts=%llu precompute=%llu marking=%llu after=%llu windows=%llu over=%llu "
+                 "dense=%llu\n", hc.prof[0], hc.prof[1], hc.prof[2], hc.prof[3], hc.dbg[0], hc.dbg[1], hc.dbg[2]);
     for (const TraceRow& t : rows)
       std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu w2cum=%llu recount=%d ms=%.3f\n", t.pid,
                    t.nF, t.t0, t.t1, t.t2, t.wedges, t.w2cum, (int)t.recount, elapsed(t.a, t.b));
