@@ -334,15 +334,18 @@ def run_ablation(args):
     for side in (0, 1):
         for name, opts in variants:
             pb.pbng_tip_decompose(d, P, side=side, opts=opts | pb.OPT_STATS)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            _, st = pb.pbng_tip_decompose(d, P, side=side, opts=opts | pb.OPT_STATS)
-            e1.record()
-            e1.synchronize()
+            secs = []
+            for _ in range(3):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                _, st = pb.pbng_tip_decompose(d, P, side=side, opts=opts | pb.OPT_STATS)
+                e1.record()
+                e1.synchronize()
+                secs.append(e0.elapsed_time(e1) / 1000)
             w = st["wedges_count"] + st["wedges_cd"] + st["wedges_fd"]
             print(json.dumps({"ablation": name, "config": workload_desc(args.config, g, P), "side": side,
-                              "seconds": e0.elapsed_time(e1) / 1000, "wedges": w,
+                              "seconds": statistics.median(secs), "seconds_all": secs, "wedges": w,
                               "wedges_count": st["wedges_count"], "wedges_cd": st["wedges_cd"],
                               "wedges_fd": st["wedges_fd"], "rho_cd_iters": st["rho_cd_iters"],
                               "recounts": st["recounts"]}), flush=True)

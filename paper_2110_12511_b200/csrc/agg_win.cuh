@@ -46,6 +46,12 @@ constexpr int kSegDepth = PBNG_SEG_DEPTH;  // 16-byte loads per lane issued toge
 #ifndef PBNG_WIN_FAST
 #define PBNG_WIN_FAST 1
 #endif
+#ifndef PBNG_COMBINE
+#define PBNG_COMBINE 0
+#endif
+#ifndef PBNG_COMBINE_DENSE
+#define PBNG_COMBINE_DENSE 0
+#endif
 #ifndef PBNG_DENSE_TOUCH
 #define PBNG_DENSE_TOUCH 1
 #endif
@@ -166,12 +172,27 @@ __device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64
 
 // Mark the entries p[i0, i1) (all inside the window starting at `a`) in the
 // bitmap; repeats go to the table.
+// Lanes of one warp step hold distinct ids of one sorted list, so in dense
+// id ranges several lanes hit the same word: with PBNG_COMBINE the lanes of a
+// word are grouped (match_any), their bits / increments combined and one lane
+// issues the atomic, instead of the shared-memory unit serialising them.
 __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
                                          uint32_t skip, WinSmem& S, WinShared& sh) {
+  const uint32_t ln = lane_id();
   auto one = [&](bool ok, uint32_t x) {
-    if (ok && x != skip) {
-      const uint32_t o = x - a;
-      const uint32_t bit = 1u << (o & 31);
+    const bool act = ok && x != skip;
+    const uint32_t o = x - a;
+    const uint32_t bit = 1u << (o & 31);
+    if (PBNG_COMBINE) {
+      const uint32_t wd = act ? o >> 5 : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(kFull, wd);
+      const uint32_t leader = __ffs(peers) - 1;
+      const uint32_t orv = __reduce_or_sync(peers, act ? bit : 0u);
+      uint32_t old = 0;
+      if (act && ln == leader) old = atomicOr(&S.bits[wd], orv);
+      old = __shfl_sync(peers, old, leader);
+      if (act && (old & bit)) win_dup_insert(S, sh, x);
+    } else if (act) {
       if (atomicOr(&S.bits[o >> 5], bit) & bit) win_dup_insert(S, sh, x);
     }
   };
@@ -197,7 +218,10 @@ template <class L, class Fn>
 __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t nl, bool pre,
                                          const uint32_t* __restrict__ bnd, uint32_t W, uint32_t k, uint64_t wa,
                                          uint64_t wb, uint64_t a, uint64_t b, const uint32_t* __restrict__ partner,
-                                         WinSmem& S, WinShared& sh, Fn& fn, uint32_t chunk = kWinChunk) {
+                                         WinSmem& S, WinShared& sh, Fn& fn, uint32_t chunk = kWinChunk,
+                                         const uint32_t* __restrict__ sub = nullptr, uint32_t sj = 0,
+                                         uint32_t sstride = 0) {
+  // sub (optional): precomputed bounds of list i's sub-window sj at sub[i * sstride + sj]
   const uint32_t tid = threadIdx.x, ln = lane_id();
   bool any = false;
   for (uint64_t bs = 0; bs < nl; bs += kWinLists) {
@@ -210,7 +234,10 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
       lists.get(e0 + i, base, len);
       const uint32_t* p = partner + base;
       uint32_t s, t;
-      if (pre) {
+      if (sub) {
+        s = sub[i * sstride + sj];
+        t = sub[i * sstride + sj + 1];
+      } else if (pre) {
         const uint32_t c0 = bnd[i * (W + 1) + k], c1 = bnd[i * (W + 1) + k + 1];
         s = a == wa ? c0 : lb_range(p, c0, c1, (uint32_t)a);
         t = b == wb ? c1 : lb_range(p, s, c1, (uint32_t)b);
@@ -280,10 +307,18 @@ __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint6
   auto one = [&](bool ok, uint32_t x) {
     bool fresh = false;
     uint32_t wd = 0;
-    if (ok && x != skip) {
-      const uint32_t o = x - a;
+    const bool act = ok && x != skip;
+    const uint32_t o = x - a;
+    const uint32_t inc = 1u << ((o & ((1u << lf) - 1)) << lb);
+    if (PBNG_COMBINE_DENSE) {
+      wd = act ? o >> lf : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(kFull, wd);
+      const uint32_t leader = __ffs(peers) - 1;
+      const uint32_t sum = __reduce_add_sync(peers, act ? inc : 0u);  // distinct fields: no carries
+      if (act && ln == leader) fresh = atomicAdd(&cnt[wd], sum) == 0u;
+    } else if (act) {
       wd = o >> lf;
-      fresh = atomicAdd(&cnt[wd], 1u << ((o & ((1u << lf) - 1)) << lb)) == 0u;
+      fresh = atomicAdd(&cnt[wd], inc) == 0u;
     }
     const uint32_t m = __ballot_sync(kFull, fresh);
     if (m) {
@@ -316,8 +351,8 @@ template <class L, class Emit, class Pass2 = NoPass2>
 __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_t e1, uint32_t skip,
                                             uint32_t idspace, uint32_t g, uint32_t G,
                                             const uint32_t* __restrict__ partner, WinSmem& S, WinShared& sh,
-                                            uint32_t* __restrict__ bnd, Emit& emit, unsigned long long* dbg,
-                                            const Pass2& pass2 = Pass2()) {
+                                            uint32_t* __restrict__ bnd, uint32_t pre_lists, Emit& emit,
+                                            unsigned long long* dbg, const Pass2& pass2 = Pass2()) {
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
   const uint64_t nl = e1 - e0;
   const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
@@ -325,12 +360,13 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   if (k0 >= k1) return;
   // fast path: every list's window bounds, base and per-window chunk prefixes
   // are computed once per start (per-CTA scratch), so a window needs no scan
-  const bool pre = nl <= kWinLists && k1 - k0 <= kWinMaxW;
+  const uint32_t PL = pre_lists;  // scratch stride (lists) of the precomputed tables
+  const bool pre = nl <= PL && k1 - k0 <= kWinMaxW;
   const uint32_t lb = dense_log_bits(nl);                 // dense counter width 2^lb bits
   const uint32_t SW = kWinBitWords << (5 - lb);           // ids per dense pass
   const uint32_t W1 = W + 1;
-  uint32_t* cpg = bnd + (uint64_t)kWinLists * W1;                        // [kr * kWinLists + i]
-  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(cpg + (uint64_t)kWinLists * W1);
+  uint32_t* cpg = bnd + (uint64_t)PL * W1;  // [kr * PL + i]
+  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(cpg + (uint64_t)PL * W1);
   const long long tp0 = clock64();
   for (uint32_t k = tid; k < kWinMaxW; k += bd) S.ek[k] = 0;
   __syncthreads();
@@ -348,7 +384,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         if (k <= k1) {
           const uint64_t key = (uint64_t)k * kWinIds;
           v = lb_range(partner + base, 0, len, key < idspace ? (uint32_t)key : idspace);
-          bnd[i * W1 + k] = v;
+          bnd[(uint64_t)i * W1 + k] = v;
         }
         uint32_t left = __shfl_up_sync(kFull, v, 1);
         if (ln == 0) left = prev;
@@ -358,12 +394,17 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     }
     __syncthreads();
     for (uint32_t k = k0; k < k1; k++) {
-      uint32_t nch = 0;
-      if (tid < nl) nch = (bnd[tid * W1 + k + 1] - bnd[tid * W1 + k] + kWinChunk - 1) / kWinChunk;
-      uint32_t tot;
-      const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
-      if (tid < nl) cpg[(k - k0) * kWinLists + tid] = cp;
-      if (tid == 0) S.ctot[k - k0] = tot;
+      uint32_t carry = 0;
+      for (uint32_t t0 = 0; t0 < nl; t0 += bd) {
+        const uint32_t i = t0 + tid;
+        uint32_t nch = 0;
+        if (i < nl) nch = (bnd[(uint64_t)i * W1 + k + 1] - bnd[(uint64_t)i * W1 + k] + kWinChunk - 1) / kWinChunk;
+        uint32_t tot;
+        const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
+        if (i < nl) cpg[(uint64_t)(k - k0) * PL + i] = carry + cp;
+        carry += tot;
+      }
+      if (tid == 0) S.ctot[k - k0] = carry;
     }
   }
   __syncthreads();
@@ -382,8 +423,11 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         sh.next = 0;
       }
       const uint32_t tot = S.ctot[kr];
-      const uint32_t* cp = cpg + (uint64_t)kr * kWinLists;
-      for (uint32_t i = tid; i < nl; i += bd) S.cpre[i] = cp[i];
+      const uint32_t* cp = cpg + (uint64_t)kr * PL;
+      const bool insm = nl <= kWinLists;  // the row fits shared memory
+      if (insm)
+        for (uint32_t i = tid; i < nl; i += bd) S.cpre[i] = cp[i];
+      const uint32_t* crow = insm ? S.cpre : cp;
       __syncthreads();
       // warps take chunks dynamically; chunk c belongs to the largest list i with cpre[i] <= c
       auto run = [&](auto&& fn) {
@@ -395,10 +439,10 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
           uint32_t lo = 0, hi = (uint32_t)nl;
           while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (S.cpre[mid] <= c) lo = mid; else hi = mid;
+            if (crow[mid] <= c) lo = mid; else hi = mid;
           }
-          const uint64_t sbeg = gbase[lo] + bnd[lo * W1 + k], send = gbase[lo] + bnd[lo * W1 + k + 1];
-          const uint64_t q0 = sbeg + (uint64_t)(c - S.cpre[lo]) * kWinChunk;
+          const uint64_t sbeg = gbase[lo] + bnd[(uint64_t)lo * W1 + k], send = gbase[lo] + bnd[(uint64_t)lo * W1 + k + 1];
+          const uint64_t q0 = sbeg + (uint64_t)(c - crow[lo]) * kWinChunk;
           fn(q0, q0 + kWinChunk < send ? q0 + kWinChunk : send, e0 + lo);
         }
       };
@@ -427,7 +471,6 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         if (!over) emit((uint32_t)(v >> 32), (uint32_t)v + 1u);
       }
       if (tid == 0) atomicAdd(&dbg[over ? 1 : 0], 1ull);
-      if (tid == 0) atomicAdd(&dbg[7], (unsigned long long)(clock64() - tm1));
       if (over) {
         for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
         dense = true;
@@ -472,8 +515,25 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       if (tid == 0) atomicAdd(&dbg[1], 1ull);
       __syncthreads();
     }
-    // dense counting in sub-windows of SW ids
+    // dense counting in sub-windows of SW ids; with tables, every list's
+    // sub-window bounds are found at once (a warp per list, a lane per bound)
+    const long long td0 = clock64();
+    const uint32_t NS = (uint32_t)((wb - wa + SW - 1) / SW);
+    uint32_t* sub = nullptr;
+    if (pre && NS <= 32) {
+      sub = reinterpret_cast<uint32_t*>(gbase + PL);  // PL * 33 entries
+      for (uint32_t i = wid; i < nl; i += nw) {
+        const uint32_t c0 = bnd[(uint64_t)i * W1 + k], c1 = bnd[(uint64_t)i * W1 + k + 1];
+        const uint32_t* p = partner + gbase[i];
+        for (uint32_t j = ln; j <= NS; j += 32) {
+          const uint64_t key = wa + (uint64_t)j * SW;
+          sub[(uint64_t)i * 33 + j] = j == 0 ? c0 : (key >= wb ? c1 : lb_range(p, c0, c1, (uint32_t)key));
+        }
+      }
+      __syncthreads();
+    }
     for (uint64_t a = wa; a < wb; a += SW) {
+      const uint32_t sj = (uint32_t)((a - wa) / SW);
       const uint64_t b = a + SW < wb ? a + SW : wb;
       uint32_t* touch = reinterpret_cast<uint32_t*>(S.dup);
       if (tid == 0) sh.ndup = 0;  // touched-word count
@@ -482,7 +542,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         dense_mark(partner, i0, i1, (uint32_t)a, skip, lb, S.bits, touch, &sh.ndup);
       };
       const uint32_t chunk = pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk;
-      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk);
+      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk, sub, sj, 33);
       if (!any) continue;
       if (Pass2::kOn) {
         auto sum = [&](uint64_t i0, uint64_t i1, uint64_t e) {
@@ -494,7 +554,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
           cs = warp_sum(cs);
           if (ln == 0 && cs) pass2(e, cs);
         };
-        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum, chunk);
+        win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum, chunk, sub, sj, 33);
       }
       const uint32_t fpw = 1u << (5 - lb);  // fields per word
       const uint32_t nwords = (uint32_t)((b - a + fpw - 1) / fpw);
@@ -519,6 +579,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     // the repeat table's memory held touched words: empty it again
     for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
     __syncthreads();
+    if (tid == 0) atomicAdd(&dbg[7], (unsigned long long)(clock64() - td0));
   }
 }
 
@@ -546,8 +607,12 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
     const long long ts0 = clock64();
-    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, out, a.c->dbg);
-    if (threadIdx.x == 0) atomicAdd(&a.c->prof[0], (unsigned long long)(clock64() - ts0));
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg);
+    if (threadIdx.x == 0) {
+      const bool tab = a.offU[u + 1] - a.offU[u] <= a.win_pre;
+      atomicAdd(tab ? &a.c->prof[0] : &a.c->prof2[0], (unsigned long long)(clock64() - ts0));
+      atomicAdd(tab ? &a.c->prof2[2] : &a.c->prof2[1], 1ull);
+    }
     if (MODE == 0) {
       acc = warp_sum(acc);
       if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);

@@ -80,7 +80,8 @@ struct Counters {
   unsigned long long cum_steps;  // Σ d_u of every traversed u ((u, v) steps)
   unsigned long long tier_wedges[3];  // Σ wl routed to each tier
   unsigned long long dbg[4];          // tier-2 internals: bitmap windows, overflows, dense passes, -
-  unsigned long long prof[4];         // tier-2 clock64 of CTA thread 0: whole starts, precompute, marking, after-marking
+  unsigned long long prof[4];         // tier-2 clock64 of CTA thread 0: starts with tables, precompute, bitmap windows, dense passes
+  unsigned long long prof2[4];        // tier-2: cycles / count of starts without tables, count of starts with tables, -
 };
 
 // ---------------------------------------------------------------- init
@@ -321,6 +322,7 @@ struct AggArgs {
   uint32_t* win_bnd;
   uint64_t win_cap;
   uint32_t win_split;                  // window groups per tier-2 start (>1 for small batches)
+  uint32_t win_pre;                    // starts with at most this many lists use precomputed window tables
 };
 
 template <int MODE>

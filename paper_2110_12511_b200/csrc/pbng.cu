@@ -19,6 +19,10 @@
 #include "kernels_relabel.cuh"
 #include "kernels_vp.cuh"
 
+#ifndef PBNG_WIN_PRE_MAX
+#define PBNG_WIN_PRE_MAX 4096
+#endif
+
 using namespace pbng;
 
 namespace {
@@ -382,6 +386,7 @@ struct State {
   uint32_t* win_bnd;  // tier-2 window bounds, win_cap per CTA
   uint64_t win_cap;
   uint32_t win_split = 1;  // window groups per tier-2 start in the next launch
+  uint32_t win_pre = 1024;
   // chunked compaction of long lists
   uint2* comp_task;
   uint32_t *comp_tbase, *comp_oldL, *comp_cnt, *comp_ntask;
@@ -468,7 +473,10 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank&
   S.piece_srange = r.alloc<uint32_t>(np);
   S.piece_pedge = vp ? r.alloc<uint64_t>(np) : nullptr;
   const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWinIds - 1) / kWinIds;
-  S.win_cap = 2 * (uint64_t)kWinLists * (wmax + 1) + 2 * (uint64_t)kWinLists;  // bounds, chunk prefixes, bases
+  // per-CTA tables of starts with up to win_pre lists: bounds + chunk prefixes
+  // ((W+1) u32 each per list) and list bases (u64); about 8 MB per CTA at most
+  S.win_pre = (uint32_t)std::max<uint64_t>(kWinLists, std::min<uint64_t>(PBNG_WIN_PRE_MAX, (8ull << 20) / (8 * (wmax + 1) + 8)));
+  S.win_cap = 2 * (uint64_t)S.win_pre * (wmax + 1) + 2 * (uint64_t)S.win_pre + 33 * (uint64_t)S.win_pre;
   S.win_bnd = r.alloc<uint32_t>((size_t)r.nsm * kWinCtas * S.win_cap);
 }
 
@@ -498,6 +506,7 @@ AggArgs agg_args(const State& S, int t) {
   a.win_bnd = S.win_bnd;
   a.win_cap = S.win_cap;
   a.win_split = S.win_split;
+  a.win_pre = S.win_pre;
   return a;
 }
 
@@ -754,8 +763,9 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
   if (plan.nparts) plan.bounds.back() = kInf;
   if (trace) {
     const Counters hc = r.readback(S.c);
-    std::fprintf(stderr, "tier2 cycles: starts=%llu precompute=%llu marking=%llu after=%llu windows=%llu over=%llu "
-                 "dense=%llu\n", hc.prof[0], hc.prof[1], hc.prof[2], hc.prof[3], hc.dbg[0], hc.dbg[1], hc.dbg[2]);
+    std::fprintf(stderr, "tier2 cycles: tabled_starts=%llu precompute=%llu bitmap=%llu dense=%llu | untabled=%llu "
+                 "n_untabled=%llu n_tabled=%llu | windows=%llu over=%llu dense_passes=%llu\n", hc.prof[0], hc.prof[1],
+                 hc.prof[2], hc.prof[3], hc.prof2[0], hc.prof2[1], hc.prof2[2], hc.dbg[0], hc.dbg[1], hc.dbg[2]);
     for (const TraceRow& t : rows)
       std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu w2cum=%llu recount=%d ms=%.3f\n", t.pid,
                    t.nF, t.t0, t.t1, t.t2, t.wedges, t.w2cum, (int)t.recount, elapsed(t.a, t.b));

@@ -1,0 +1,10 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 600 python -m pytest tests -m gpu -x -q -k "not config4 and not config5" > gpurun_out/r23_pytest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/r23_pytest.log
+for v in p32k p4k p32knt; do
+  for c in 3 4 5; do
+    PBNG_TRACE=1 PBNG_LIB=paper_2110_12511_b200/libpbng_$v.so timeout 300 python scripts/quick_run.py $c --opts 8 --reps $([ $c = 5 ] && echo 1 || echo 2) 2>&1 | grep -v "^cd \|^fd " > gpurun_out/r23_${v}_$c.log
+  done
+done
+for f in gpurun_out/r23_p*.log; do echo $f; grep -h "tier2" $f | tail -1 | cut -c1-250; grep -h "rep" $f | tail -1 | cut -c1-250; done
