@@ -52,8 +52,11 @@ constexpr int kSegDepth = PBNG_SEG_DEPTH;  // 16-byte loads per lane issued toge
 #ifndef PBNG_COMBINE_DENSE
 #define PBNG_COMBINE_DENSE 0
 #endif
+#ifndef PBNG_DENSE_CHUNK
+#define PBNG_DENSE_CHUNK 1024
+#endif
 #ifndef PBNG_DENSE_TOUCH
-#define PBNG_DENSE_TOUCH 1
+#define PBNG_DENSE_TOUCH 0
 #endif
 constexpr uint32_t kWinChunk = PBNG_WIN_CHUNK ? PBNG_WIN_CHUNK : 512;  // entries per warp task
 
@@ -316,6 +319,9 @@ __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint6
       const uint32_t leader = __ffs(peers) - 1;
       const uint32_t sum = __reduce_add_sync(peers, act ? inc : 0u);  // distinct fields: no carries
       if (act && ln == leader) fresh = atomicAdd(&cnt[wd], sum) == 0u;
+    } else if (!PBNG_DENSE_TOUCH) {
+      if (act) atomicAdd(&cnt[o >> lf], inc);  // no touched list: the sweep reads every word
+      return;
     } else if (act) {
       wd = o >> lf;
       fresh = atomicAdd(&cnt[wd], inc) == 0u;
@@ -377,6 +383,22 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       uint32_t len;
       lists.get(e0 + i, base, len);
       if (ln == 0) gbase[i] = base;
+      if (len <= 32) {
+        // short list: one coalesced load, every bound by a ballot count
+        const uint32_t x = ln < len ? partner[base + ln] : 0xFFFFFFFFu;
+        uint32_t prev = 0;
+        for (uint32_t k = k0; k <= k1; k++) {
+          const uint64_t key = (uint64_t)k * kWinIds;
+          const uint32_t kk = key < idspace ? (uint32_t)key : idspace;
+          const uint32_t v = __popc(__ballot_sync(kFull, x < kk));
+          if (ln == 0) {
+            bnd[(uint64_t)i * W1 + k] = v;
+            if (k > k0 && v > prev) atomicAdd(&S.ek[k - 1 - k0], (unsigned long long)(v - prev));
+          }
+          prev = v;
+        }
+        continue;
+      }
       uint32_t prev = 0;
       for (uint32_t kb = k0; kb <= k1; kb += 32) {
         const uint32_t k = kb + ln;
@@ -541,7 +563,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) {
         dense_mark(partner, i0, i1, (uint32_t)a, skip, lb, S.bits, touch, &sh.ndup);
       };
-      const uint32_t chunk = pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk;
+      const uint32_t chunk = PBNG_DENSE_CHUNK ? PBNG_DENSE_CHUNK : (pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk);
       const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk, sub, sj, 33);
       if (!any) continue;
       if (Pass2::kOn) {
