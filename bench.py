@@ -28,7 +28,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "tip-decomposition wedges/sec"
 UNIT = "wedges/s"
-DEFAULT_CONFIG = "4"
+DEFAULT_CONFIG = "5"  # the largest config (BASELINE.json north_star: the HBM target is stated on it)
 
 
 def log(*a):
@@ -45,10 +45,23 @@ def locked_build():
 
 
 def load_graph(cfg):
+    """Seeded synthetic workload.  Configs >= 4 are cached on local disk (outside
+    any timed region) so replicas / reruns skip the minute-long generation; the
+    file name carries the generator version, and one process writes it under a lock."""
     import graphgen as gg
     c = cfg if cfg == "2a" else int(cfg)
     t = time.time()
-    g, P = gg.config(c, cache_dir=os.environ.get("PBNG_CACHE"))
+    cache = os.environ.get("PBNG_CACHE")
+    if cache is None and c not in ("2a",) and int(c) >= 4:
+        cache = os.path.join("/tmp", f"pbng_graph_cache_{gg.GENERATOR_VERSION}")
+    if cache:
+        os.makedirs(cache, exist_ok=True)
+        with open(os.path.join(cache, f".lock{c}"), "w") as lf:
+            fcntl.flock(lf, fcntl.LOCK_EX)
+            g, P = gg.config(c, cache_dir=cache)
+            fcntl.flock(lf, fcntl.LOCK_UN)
+    else:
+        g, P = gg.config(c)
     return g, P, time.time() - t
 
 
@@ -261,13 +274,13 @@ def run_gpu(args):
                for a, dt in ((g.off_u, np.int64), (g.adj_u, np.int32), (g.off_v, np.int64), (g.adj_v, np.int32))]
         hv = [p.numpy() for p in pin]
         tip_host = torch.empty(g.nU, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-        pb.pbng_tip_decompose_host(hv[0].view(np.uint64), hv[1].view(np.uint32), hv[2].view(np.uint64),
-                                   hv[3].view(np.uint32), P, out=tip_host)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        # the device path above already warmed every kernel and the memory pool
+        e2e_steps = min(args.steps, 2)
         e2e_ms = 0.0
-        for i in range(args.steps):
+        for i in range(e2e_steps):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -277,10 +290,10 @@ def run_gpu(args):
             e1.synchronize()
             e2e_ms += e0.elapsed_time(e1)
         e2e_max = max_over_ranks(e2e_ms, dist, device=f"cuda:{local}")
-        e2e = {"value": job_rate(wedges_step * args.steps, world, e2e_max), "unit": UNIT,
+        e2e = {"value": job_rate(wedges_step * e2e_steps, world, e2e_max), "unit": UNIT,
                "h2d_bytes_per_step": int(sum(p.numel() * p.element_size() for p in pin)),
                "d2h_bytes_per_step": int(g.nU * 8),
-               "seconds_per_decomposition": e2e_max / 1000 / args.steps,
+               "seconds_per_decomposition": e2e_max / 1000 / e2e_steps, "steps": e2e_steps,
                "api": "pbng_tip_decompose_host (C ABI, pinned host buffers)"}
     if rank != 0:
         if dist:

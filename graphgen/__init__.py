@@ -208,6 +208,9 @@ def peel_side_cheaper(g: Graph) -> str:
     return "U" if cost_u <= cost_v else "V"
 
 
+GENERATOR_VERSION = "r1"  # bump when any generator changes (names the on-disk cache)
+
+
 def config(cfg, cache_dir: str | None = None) -> tuple[Graph, int]:
     """Build BASELINE config `cfg`; returns (graph oriented so that U is the peel side, P)."""
     spec = CONFIGS[cfg]
@@ -223,7 +226,9 @@ def config(cfg, cache_dir: str | None = None) -> tuple[Graph, int]:
         g.name = f"cfg{cfg}"
         if path:
             os.makedirs(cache_dir, exist_ok=True)
-            np.savez(path, nU=g.nU, nV=g.nV, off_u=g.off_u, adj_u=g.adj_u, off_v=g.off_v, adj_v=g.adj_v)
+            tmp = path[:-4] + f".tmp{os.getpid()}.npz"  # complete file or none
+            np.savez(tmp, nU=g.nU, nV=g.nV, off_u=g.off_u, adj_u=g.adj_u, off_v=g.off_v, adj_v=g.adj_v)
+            os.replace(tmp, path)
     side = spec["side"]
     if side == "cheaper":
         side = peel_side_cheaper(g)
@@ -232,5 +237,5 @@ def config(cfg, cache_dir: str | None = None) -> tuple[Graph, int]:
     return g, spec["P"]
 
 
-__all__ = ["Graph", "uniform", "chung_lu", "blocks", "block_sizes", "from_edges", "complete", "config",
+__all__ = ["GENERATOR_VERSION", "Graph", "uniform", "chung_lu", "blocks", "block_sizes", "from_edges", "complete", "config",
            "CONFIGS", "peel_side_cheaper", "build_lib"]

@@ -415,6 +415,23 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       }
     }
     __syncthreads();
+    if (nl <= 32) {
+      // few lists: one warp scans every window's chunk counts (no CTA barriers)
+      if (wid == 0) {
+        for (uint32_t k = k0; k < k1; k++) {
+          const uint32_t nch = ln < nl ? (bnd[(uint64_t)ln * W1 + k + 1] - bnd[(uint64_t)ln * W1 + k] +
+                                          kWinChunk - 1) / kWinChunk : 0u;
+          uint32_t incl = nch;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (ln >= (uint32_t)o) incl += y;
+          }
+          if (ln < nl) cpg[(uint64_t)(k - k0) * PL + ln] = incl - nch;
+          if (ln == 31) S.ctot[k - k0] = incl;
+        }
+      }
+    } else
     for (uint32_t k = k0; k < k1; k++) {
       uint32_t carry = 0;
       for (uint32_t t0 = 0; t0 < nl; t0 += bd) {
