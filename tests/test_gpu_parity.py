@@ -96,7 +96,7 @@ def test_config3_parity(pb):
     tip, st = pb.pbng_tip_decompose(d, P)
     want_sup = oracle.count(g)
     assert np.array_equal(sup, want_sup)
-    want = oracle.bup_tip(g)
+    want = _config3_theta(g)
     assert np.array_equal(pb.as_u64(tip), want)
     assert st["partitions_used"] > 1
     part, init, bounds, nparts = pb.pbng_tip_plan(d, P)
@@ -243,3 +243,32 @@ def test_config5_sampled_certificate(pb):
     assert np.all(oracle.cert_support_ge(g, th, us) >= th[us])
     bad, first = oracle.cert_levels(g, th, _sample_levels(th, rng))
     assert bad == 0, first
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_tip_other_side(pb, cfg):
+    """Peeling the other vertex side (side=1 swaps the roles of U and V)."""
+    g, P = gg.config(cfg)
+    gs = g.swapped()
+    d = dev(pb, g)
+    assert np.array_equal(pb.as_u64(pb.pbng_count_butterflies(d, side=1)), oracle.count(gs))
+    tip, st = pb.pbng_tip_decompose(d, P, side=1)
+    assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs))
+
+
+@pytest.mark.parametrize("P", [1, 7, 64, 400])
+def test_config3_partition_counts(pb, P):
+    """Config 3 with P from 1 (all of U peeled by FD = BUP) to 400: θ does not depend on P."""
+    g, _ = gg.config(3)
+    tip, st = pb.pbng_tip_decompose(dev(pb, g), P)
+    assert np.array_equal(pb.as_u64(tip), _config3_theta(g))
+    assert 1 <= st["partitions_used"] <= P
+
+
+_C3 = {}
+
+
+def _config3_theta(g):
+    if "theta" not in _C3:
+        _C3["theta"] = oracle.bup_tip(g)
+    return _C3["theta"]
