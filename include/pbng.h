@@ -74,7 +74,8 @@ typedef struct {
   uint64_t updates_fd;       /* support decrements applied in FD (included in support_updates) */
   uint32_t launches;         /* kernels launched by this call */
   uint32_t pad;
-  uint64_t impl[4];          /* implementation counters (tier-1 ranges, replays, -, pieces walked) */
+  uint64_t impl[4];          /* implementation counters (tier-2 bitmap windows, repeat-table overflows,
+                                dense passes, -) */
   /* device time per kernel family, filled only with PBNG_OPT_STATS (CUDA events
    * recorded on `stream` around each launch): index by PBNG_K_* */
   float ms_kernel[16];
@@ -84,8 +85,8 @@ enum {
   PBNG_K_INIT = 0,      /* k_init_u / k_init_v / validation */
   PBNG_K_CLASSIFY = 1,  /* k_classify: per-vertex wedge work and tier routing */
   PBNG_K_AGG_WARP = 2,  /* k_agg_warp: tier-0 wedge aggregation (warp per vertex) */
-  PBNG_K_AGG_CTA = 3,   /* k_agg_range: tier-1 wedge aggregation (CTA per vertex, range-partitioned hash) */
-  PBNG_K_AGG_HEAVY = 4, /* k_agg_heavy: tier-2 wedge aggregation (dense global counters) */
+  PBNG_K_AGG_CTA = 3,   /* k_agg_mid / k_agg_win (+ vertex-priority variants): CTA-per-start aggregation */
+  PBNG_K_AGG_HEAVY = 4, /* (unused) */
   PBNG_K_SELECT = 5,    /* k_select: frontier selection + compaction */
   PBNG_K_RANGE = 6,     /* k_range_hist: ⋈^init snapshot + range histogram */
   PBNG_K_COMPACT = 7,   /* k_compact*: dynamic deletion */
@@ -109,8 +110,10 @@ enum {
   PBNG_OPT_VALIDATE = 4,       /* O(m) CSR precondition check -> PBNG_ERR_GRAPH */
   PBNG_OPT_STATS = 8,          /* count wedges / updates on device (small overhead) */
   PBNG_OPT_FORCE_RECOUNT = 16, /* test hook: take the re-count branch every CD iteration */
-  PBNG_OPT_ONESIDED_COUNT = 32 /* count (and re-count) by one-sided wedge aggregation, W = Σ_v d_v^2
-                                  (P:369-373), instead of vertex-priority counting (Alg.1) */
+  PBNG_OPT_ONESIDED_COUNT = 32, /* count (and re-count) by one-sided wedge aggregation, W = Σ_v d_v^2
+                                   (P:369-373), instead of vertex-priority counting (Alg.1) */
+  PBNG_OPT_FD_GRID = 64         /* test hook: peel every FD partition of <= 4096 members on the whole GPU
+                                   (by default only partitions with far above average work) */
 };
 
 /* Per-vertex butterfly counts of the peel side:

@@ -28,6 +28,7 @@ LIB_PATH = os.environ.get("PBNG_LIB") or os.path.join(_HERE, "libpbng.so")
 
 OK, ERR_ARG, ERR_GRAPH, ERR_OOM, ERR_CUDA = 0, 1, 2, 3, 4
 OPT_NO_RECOUNT, OPT_NO_DELETE, OPT_VALIDATE, OPT_STATS, OPT_FORCE_RECOUNT, OPT_ONESIDED_COUNT = 1, 2, 4, 8, 16, 32
+OPT_FD_GRID = 64
 MAX_P = 4096
 KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_heavy", "select", "range", "compact",
                    "fd_build", "fd", "count_vp")

@@ -43,6 +43,10 @@ constexpr uint32_t kWinDupCap = kWinDupSlots / 2;
 #define PBNG_SEG_DEPTH 1
 #endif
 constexpr int kSegDepth = PBNG_SEG_DEPTH;  // 16-byte loads per lane issued together
+#ifndef PBNG_DENSE_DEPTH
+#define PBNG_DENSE_DEPTH 1
+#endif
+constexpr int kDenseDepth = PBNG_DENSE_DEPTH;
 #ifndef PBNG_WIN_FAST
 #define PBNG_WIN_FAST 1
 #endif
@@ -140,7 +144,7 @@ __device__ __forceinline__ uint32_t lb_range(const uint32_t* __restrict__ p, uin
 // warp-convergently (ok = the lane holds an entry).  The 16-byte aligned body is
 // read 512 entries per step, four independent 16-byte loads per lane issued
 // before any entry is used, so each warp keeps 2 KB of loads in flight.
-template <class Fn>
+template <int D = kSegDepth, class Fn>
 __device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, Fn& fn) {
   const uint32_t ln = lane_id();
   uint64_t h = (i0 + 3) & ~3ull;  // first 16-byte aligned index
@@ -150,17 +154,17 @@ __device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64
     fn(ok, ok ? p[i0 + ln] : 0u);
   }
   const uint64_t t = h + ((i1 - h) & ~3ull);  // end of the aligned body
-  for (uint64_t q0 = h; q0 < t; q0 += 128 * kSegDepth) {
-    uint4 v[kSegDepth];
-    bool ok[kSegDepth];
+  for (uint64_t q0 = h; q0 < t; q0 += 128 * D) {
+    uint4 v[D];
+    bool ok[D];
 #pragma unroll
-    for (int j = 0; j < kSegDepth; j++) {
+    for (int j = 0; j < D; j++) {
       const uint64_t q = q0 + 128 * j + 4 * ln;
       ok[j] = q < t;
       v[j] = ok[j] ? __ldg(reinterpret_cast<const uint4*>(p + q)) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int j = 0; j < kSegDepth; j++) {
+    for (int j = 0; j < D; j++) {
       fn(ok[j], v[j].x);
       fn(ok[j], v[j].y);
       fn(ok[j], v[j].z);
@@ -336,7 +340,7 @@ __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint6
       if (fresh && slot < kTouchCap) touch[slot] = wd;
     }
   };
-  seg_visit(p, i0, i1, one);
+  seg_visit<kDenseDepth>(p, i0, i1, one);
 }
 __device__ __forceinline__ uint32_t dense_get(const uint32_t* cnt, uint32_t o, uint32_t lb) {
   const uint32_t lf = 5 - lb, bits = 1u << lb;

@@ -573,3 +573,142 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
 }
 
 }  // namespace pbng
+
+namespace pbng {
+
+// ---------------------------------------------------------------- FD on the grid
+// A partition whose FD work is far above the average but whose members are few
+// (the densest core, highest tip numbers) would keep one SM busy long after the
+// others finished.  It is peeled instead in host-driven rounds that use every
+// SM: the same level-synchronous rule (level k = max(k, min live support);
+// peel every live member with support <= k), with the wedges of the selected
+// members spread over all CTAs and w counted per (selected, member) pair in
+// shared memory, indexed by the member's position in the partition.
+constexpr uint32_t kGridCnt = 36864;  // (selected x members) counters per CTA (144 KB)
+constexpr uint32_t kGridMaxMembers = 4096;
+constexpr uint32_t kGridThreads = 512;
+
+// lpos[members[i]] = i
+__global__ void k_fdg_pos(const uint32_t* __restrict__ members, uint32_t n, uint32_t* __restrict__ lpos) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) lpos[members[i]] = i;
+}
+
+// One CTA: select up to maxsel live members with support <= k (θ = k), and the
+// prefix of their degrees.  ctl = {level, nsel, total edges}.
+__global__ void __launch_bounds__(1024) k_fdg_select(const uint32_t* __restrict__ members, uint32_t n,
+                                                     const uint64_t* __restrict__ offU, uint64_t* s,
+                                                     uint32_t* state, uint64_t* theta, uint32_t maxsel,
+                                                     uint32_t* sel, uint64_t* selpre, unsigned long long* ctl) {
+  __shared__ unsigned long long s_min;
+  __shared__ uint32_t s_n, s_scan[33];
+  if (threadIdx.x == 0) {
+    s_min = ~0ull;
+    s_n = 0;
+  }
+  __syncthreads();
+  uint64_t mn = ~0ull;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t u = members[i];
+    if (state[u] == 0) mn = s[u] < mn ? s[u] : mn;
+  }
+  mn = warp_min_u64(mn);
+  if (lane_id() == 0) atomicMin(&s_min, (unsigned long long)mn);
+  __syncthreads();
+  if (s_min == ~0ull) {
+    if (threadIdx.x == 0) ctl[1] = 0;
+    return;
+  }
+  const uint64_t k = s_min > ctl[0] ? s_min : ctl[0];
+  for (uint32_t i0 = 0; i0 < n; i0 += blockDim.x) {
+    const uint32_t i = i0 + threadIdx.x;
+    const uint32_t u = i < n ? members[i] : 0u;
+    bool take = i < n && state[u] == 0 && s[u] <= k;
+    const uint32_t m = __ballot_sync(kFull, take);
+    uint32_t base = 0;
+    const uint32_t leader = m ? __ffs(m) - 1 : 0;
+    if (m && lane_id() == leader) base = atomicAdd(&s_n, (uint32_t)__popc(m));
+    base = __shfl_sync(kFull, base, leader);
+    const uint32_t slot = base + __popc(m & lanemask_lt());
+    if (take && slot < maxsel) {
+      sel[slot] = u;
+      state[u] = 3;
+      theta[u] = k;
+    }
+  }
+  __syncthreads();
+  const uint32_t ns = s_n < maxsel ? s_n : maxsel;
+  // degree prefix of the selected members (ns <= blockDim)
+  const uint32_t d = threadIdx.x < ns ? (uint32_t)(offU[sel[threadIdx.x] + 1] - offU[sel[threadIdx.x]]) : 0u;
+  uint32_t tot;
+  const uint32_t pre = block_excl_scan(d, s_scan, &tot);
+  if (threadIdx.x < ns) selpre[threadIdx.x] = pre;
+  if (threadIdx.x == 0) {
+    selpre[ns] = tot;
+    ctl[0] = k;
+    ctl[1] = ns;
+    ctl[2] = tot;
+  }
+}
+
+// All CTAs: w(selected j, member l) over the selected members' wedges inside G_p.
+__global__ void __launch_bounds__(kGridThreads) k_fdg_agg(const uint32_t* __restrict__ sel, const uint64_t* __restrict__ selpre,
+                                                          uint32_t nsel, uint32_t psz, const uint64_t* __restrict__ offU,
+                                                          const uint32_t* __restrict__ adjU,
+                                                          const uint64_t* __restrict__ offV,
+                                                          const uint64_t* __restrict__ seg,
+                                                          const uint32_t* __restrict__ adjL,
+                                                          const uint32_t* __restrict__ lpos,
+                                                          const uint32_t* __restrict__ state, uint32_t* gcnt,
+                                                          unsigned long long* wedges) {
+  extern __shared__ uint32_t cnt[];
+  __shared__ uint64_t s_pre[1025];
+  const uint32_t nc = nsel * psz;
+  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) cnt[i] = 0;
+  for (uint32_t i = threadIdx.x; i <= nsel; i += blockDim.x) s_pre[i] = selpre[i];
+  __syncthreads();
+  const uint64_t total = s_pre[nsel];
+  const FdLists L{adjU, offV, seg};
+  unsigned long long wl = 0;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = nsel;  // selected member j: s_pre[j] <= t < s_pre[j + 1]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t u = sel[lo];
+    uint64_t base;
+    uint32_t len;
+    L.get(offU[u] + (t - s_pre[lo]), base, len);
+    wl += len;
+    for (uint32_t q = 0; q < len; q++) {
+      const uint32_t x = adjL[base + q];
+      if (x == u) continue;
+      const uint32_t l = lpos[x];
+      if (l != 0xFFFFFFFFu && state[x] == 0) atomicAdd(&cnt[lo * psz + l], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&gcnt[i], cnt[i]);
+  wl = warp_sum(wl);
+  if (lane_id() == 0 && wl) atomicAdd(wedges, wl);
+}
+
+// Apply the decrements C(w, 2) of this round and clear the counters.
+__global__ void k_fdg_apply(uint32_t nc, uint32_t psz, const uint32_t* __restrict__ members, uint32_t* gcnt, uint64_t* s,
+                            unsigned long long* updates) {
+  unsigned long long upd = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    const uint32_t w = gcnt[i];
+    if (!w) continue;
+    gcnt[i] = 0;
+    if (w >= 2) {
+      atomicAdd((unsigned long long*)&s[members[i % psz]], (unsigned long long)(0ull - choose2(w)));
+      upd++;
+    }
+  }
+  upd = warp_sum(upd);
+  if (lane_id() == 0 && upd) atomicAdd(updates, upd);
+}
+
+}  // namespace pbng

@@ -84,6 +84,7 @@ void set_attrs_once() {
     cudaFuncSetAttribute(k_vp_agg_range<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
     cudaFuncSetAttribute(k_range_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem());
     cudaFuncSetAttribute(k_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem());
+    cudaFuncSetAttribute(k_fdg_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kGridCnt * 4));
     cudaGetLastError();
   });
 }
@@ -773,7 +774,48 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
 }
 
 // Fine-grained decomposition -> theta.
-void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st, float& ms_build) {
+// FD of heavy small partitions on the whole GPU, host-driven rounds (kernels_fd.cuh).
+void fd_grid(Run& r, State& S, const std::vector<uint32_t>& heavy, const std::vector<uint32_t>& hoff,
+             const std::vector<uint32_t>& hcount, const uint32_t* members, const uint64_t* seg, uint32_t* fstate,
+             uint64_t* theta, unsigned long long* fdc) {
+  uint32_t* lpos = r.alloc<uint32_t>(S.g.nU);
+  uint32_t* sel = r.alloc<uint32_t>(1024);
+  uint64_t* selpre = r.alloc<uint64_t>(1025);
+  uint32_t* gcnt = r.alloc<uint32_t>(kGridCnt);
+  unsigned long long* ctl = r.alloc<unsigned long long>(3);
+  CK(cudaMemsetAsync(lpos, 0xFF, (size_t)S.g.nU * 4, r.st));
+  CK(cudaMemsetAsync(gcnt, 0, (size_t)kGridCnt * 4, r.st));
+  for (uint32_t p : heavy) {
+    const uint32_t n = hcount[p];
+    const uint32_t* mem = members + hoff[p];
+    const uint32_t maxsel = std::min<uint32_t>(1024, kGridCnt / n);
+    r.pre(PBNG_K_FD);
+    k_fdg_pos<<<(n + 255) / 256, 256, 0, r.st>>>(mem, n, lpos);
+    r.post(PBNG_K_FD);
+    CK(cudaMemsetAsync(ctl, 0, 24, r.st));
+    for (;;) {
+      r.pre(PBNG_K_FD);
+      k_fdg_select<<<1, 1024, 0, r.st>>>(mem, n, S.g.offU, S.support, fstate, theta, maxsel, sel, selpre, ctl);
+      r.post(PBNG_K_FD);
+      unsigned long long hc[3];
+      CK(cudaMemcpyAsync(hc, ctl, 24, cudaMemcpyDeviceToHost, r.st));
+      CK(cudaStreamSynchronize(r.st));
+      const uint32_t ns = (uint32_t)hc[1];
+      if (ns == 0) break;
+      const uint32_t nc = ns * n;
+      r.pre(PBNG_K_FD);
+      k_fdg_agg<<<r.nsm * 2, kGridThreads, (size_t)nc * 4, r.st>>>(sel, selpre, ns, n, S.g.offU, S.g.adjU, S.g.offV,
+                                                                 seg, S.adjL, lpos, fstate, gcnt, fdc);
+      r.post(PBNG_K_FD);
+      r.pre(PBNG_K_FD);
+      k_fdg_apply<<<std::max<uint32_t>(1, std::min<uint32_t>((nc + 255) / 256, r.nsm * 4)), 256, 0, r.st>>>(
+          nc, n, mem, gcnt, S.support, fdc + 1);
+      r.post(PBNG_K_FD);
+    }
+  }
+}
+
+void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st, float& ms_build, uint32_t opts) {
   const uint32_t np = plan.nparts, nU = S.g.nU;
   cudaEvent_t e0 = r.event();
   uint32_t* pcount = r.alloc<uint32_t>(2 * np);  // [0, np) FD members, [np, 2np) all vertices
@@ -827,10 +869,20 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   S.slot_dup = r.alloc<uint32_t>(slot_elems);
   CK(cudaMemsetAsync(S.slot_cnt, 0, slot_elems * 4, r.st));
   // workload-aware scheduling: LPT order
-  std::vector<uint32_t> ord(np);
-  for (uint32_t i = 0; i < np; i++) ord[i] = i;
-  std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return hwork[a] > hwork[b]; });
-  CK(cudaMemcpyAsync(order, ord.data(), (size_t)np * 4, cudaMemcpyHostToDevice, r.st));
+  std::vector<uint32_t> all(np), ord, heavy;
+  for (uint32_t i = 0; i < np; i++) all[i] = i;
+  std::stable_sort(all.begin(), all.end(), [&](uint32_t a, uint32_t b) { return hwork[a] > hwork[b]; });
+  // heavy small partitions (work far above the per-SM average, few members) go to the grid path
+  unsigned long long wsum = 0;
+  for (uint32_t i = 0; i < np; i++) wsum += hwork[i];
+  const bool force_grid = (opts & PBNG_OPT_FD_GRID) != 0;
+  for (uint32_t p : all) {
+    const bool small = hcount[p] >= 1 && hcount[p] <= kGridMaxMembers;
+    if (small && (force_grid || (double)hwork[p] > 4.0 * (double)wsum / (double)r.nsm)) heavy.push_back(p);
+    else ord.push_back(p);
+  }
+  if (!ord.empty())
+    CK(cudaMemcpyAsync(order, ord.data(), (size_t)ord.size() * 4, cudaMemcpyHostToDevice, r.st));
   CK(cudaMemcpyAsync(S.support, S.init, (size_t)nU * 8, cudaMemcpyDeviceToDevice, r.st));
   cudaEvent_t e1 = r.event();
   FdArgs a;
@@ -843,7 +895,7 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
   a.poff = poff;
   a.pall = pcount + np;
   a.order = order;
-  a.nparts = np;
+  a.nparts = (uint32_t)ord.size();
   a.ticket = misc;
   a.members = members;
   a.sel = sel;
@@ -868,9 +920,12 @@ void run_fd(Run& r, State& S, const Plan& plan, uint64_t* theta, pbng_stats& st,
     CK(cudaMemsetAsync(a.ptrace, 0, (size_t)64 * np, r.st));
   }
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>({np, (uint32_t)r.nsm, S.nslots}));
-  r.pre(PBNG_K_FD);
-  k_fd<<<grid, kFdThreads, fd_smem(), r.st>>>(a);
-  r.post(PBNG_K_FD);
+  if (a.nparts) {
+    r.pre(PBNG_K_FD);
+    k_fd<<<grid, kFdThreads, fd_smem(), r.st>>>(a);
+    r.post(PBNG_K_FD);
+  }
+  if (!heavy.empty()) fd_grid(r, S, heavy, hoff, hcount, members, seg, fstate, theta, fdc);
   cudaEvent_t e2 = r.event();
   unsigned long long hf[3];
   uint32_t hm[2];
@@ -970,7 +1025,7 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   if (out.tip) {
     float ms_build = 0;
     uint64_t* theta = r.alloc<uint64_t>(g.nU);
-    run_fd(r, S, plan, theta, st, ms_build);
+    run_fd(r, S, plan, theta, st, ms_build, opts);
     st.ms_fd_build = ms_build;
     r.pre(PBNG_K_INIT);
     k_gather<uint64_t><<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, theta, out.tip);

@@ -272,3 +272,21 @@ def _config3_theta(g):
     if "theta" not in _C3:
         _C3["theta"] = oracle.bup_tip(g)
     return _C3["theta"]
+
+
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_fd_grid_path_tiny(pb, P):
+    """FD on the whole GPU (host-driven rounds), forced for every small partition."""
+    for g in tiny_corpus(60, 4000 + P):
+        d = dev(pb, g)
+        for side, gs in ((0, g), (1, g.swapped())):
+            tip, _ = pb.pbng_tip_decompose(d, P, side=side, opts=pb.OPT_FD_GRID)
+            assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(gs)), (g.name, side, P)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_fd_grid_path_configs(pb, cfg):
+    g, P = gg.config(cfg)
+    want = _config3_theta(g) if cfg == 3 else oracle.bup_tip(g)
+    tip, st = pb.pbng_tip_decompose(dev(pb, g), 400 if cfg == 3 else P, opts=pb.OPT_FD_GRID)
+    assert np.array_equal(pb.as_u64(tip), want)
