@@ -44,7 +44,7 @@ constexpr uint32_t kWinDupCap = kWinDupSlots / 2;
 #endif
 constexpr int kSegDepth = PBNG_SEG_DEPTH;  // 16-byte loads per lane issued together
 #ifndef PBNG_DENSE_DEPTH
-#define PBNG_DENSE_DEPTH 1
+#define PBNG_DENSE_DEPTH 4
 #endif
 constexpr int kDenseDepth = PBNG_DENSE_DEPTH;
 #ifndef PBNG_WIN_FAST
@@ -206,6 +206,13 @@ __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_
   seg_visit(p, i0, i1, one);
 }
 
+// Zero the first nwords words of the window array with 16-byte stores (whole CTA).
+__device__ __forceinline__ void win_clear(uint32_t* bits, uint32_t nwords) {
+  uint4* b4 = reinterpret_cast<uint4*>(bits);
+  const uint32_t n4 = (nwords + 3) >> 2;  // the array holds a multiple of 4 words
+  for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) b4[i] = make_uint4(0, 0, 0, 0);
+}
+
 // Σ repeats of the entries p[i0, i1) (pass 2 of vertex-priority counting)
 __device__ __forceinline__ unsigned long long win_sum(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1,
                                                       uint32_t skip, const WinSmem& S) {
@@ -362,7 +369,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
                                             uint32_t idspace, uint32_t g, uint32_t G,
                                             const uint32_t* __restrict__ partner, WinSmem& S, WinShared& sh,
                                             uint32_t* __restrict__ bnd, uint32_t pre_lists, Emit& emit,
-                                            unsigned long long* dbg, const Pass2& pass2 = Pass2()) {
+                                            unsigned long long* dbg, bool prof, const Pass2& pass2 = Pass2()) {
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
   const uint64_t nl = e1 - e0;
   const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
@@ -451,7 +458,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     }
   }
   __syncthreads();
-  if (tid == 0) atomicAdd(&dbg[5], (unsigned long long)(clock64() - tp0));
+  if (prof && tid == 0) atomicAdd(&dbg[5], (unsigned long long)(clock64() - tp0));
   for (uint32_t k = k0; k < k1; k++) {
     const uint64_t wa = (uint64_t)k * kWinIds;
     const uint64_t wb = wa + kWinIds < idspace ? wa + kWinIds : idspace;
@@ -493,7 +500,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       __syncthreads();
       const long long tm1 = clock64();
-      if (tid == 0) atomicAdd(&dbg[6], (unsigned long long)(tm1 - tm0));
+      if (prof && tid == 0) atomicAdd(&dbg[6], (unsigned long long)(tm1 - tm0));
       const bool over = sh.over != 0;
       const uint32_t nd = min(sh.ndup, kWinDupCap);
       if (Pass2::kOn && !over && nd) {
@@ -506,7 +513,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         __syncthreads();
       }
       const uint32_t nwords = (uint32_t)((wb - wa + 31) >> 5);
-      for (uint32_t i = tid; i < nwords; i += bd) S.bits[i] = 0;
+      win_clear(S.bits, nwords);
       for (uint32_t i = tid; i < nd; i += bd) {
         const uint32_t sl = S.dslot[i];
         const unsigned long long v = S.dup[sl];
@@ -541,7 +548,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       }
       if (any) {
         const uint32_t nwords = (uint32_t)((wb - wa + 31) >> 5);
-        for (uint32_t i = tid; i < nwords; i += bd) S.bits[i] = 0;
+        win_clear(S.bits, nwords);
         for (uint32_t i = tid; i < nd; i += bd) {
           const uint32_t sl = S.dslot[i];
           const unsigned long long v = S.dup[sl];
@@ -603,16 +610,39 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       const uint32_t nwords = (uint32_t)((b - a + fpw - 1) / fpw);
       const uint32_t nt = sh.ndup;
       const bool listed = PBNG_DENSE_TOUCH && nt <= kTouchCap;
-      for (uint32_t t = tid; t < (listed ? nt : nwords); t += bd) {
-        const uint32_t i = listed ? touch[t] : t;
-        const uint32_t v = S.bits[i];
-        if (v) {
-          S.bits[i] = 0;
-          const uint32_t bits = 1u << lb;
-          const uint32_t mask = bits == 32 ? 0xFFFFFFFFu : (1u << bits) - 1;
-          for (uint32_t f = 0; f < fpw; f++) {
-            const uint32_t c = (v >> (f << lb)) & mask;
-            if (c >= 2) emit((uint32_t)a + i * fpw + f, c);
+      // fields with count >= 2 have a bit above their lowest bit set: find them
+      // with one mask per word and visit only those
+      const uint32_t bits = 1u << lb;
+      const uint32_t fmask = bits == 32 ? 0xFFFFFFFFu : (1u << bits) - 1;
+      const uint32_t lows = lb == 1 ? 0x55555555u : lb == 2 ? 0x11111111u : lb == 3 ? 0x01010101u
+                          : lb == 4 ? 0x00010001u : 0x00000001u;
+      auto sweep_word = [&](uint32_t i, uint32_t v) {
+        uint32_t m = v & ~lows;
+        while (m) {
+          const uint32_t f = (uint32_t)(__ffs(m) - 1) >> lb;
+          emit((uint32_t)a + i * fpw + f, (v >> (f << lb)) & fmask);
+          m &= ~(fmask << (f << lb));
+        }
+      };
+      if (listed) {
+        for (uint32_t t = tid; t < nt; t += bd) {
+          const uint32_t i = touch[t];
+          const uint32_t v = S.bits[i];
+          if (v) {
+            S.bits[i] = 0;
+            sweep_word(i, v);
+          }
+        }
+      } else {
+        uint4* b4 = reinterpret_cast<uint4*>(S.bits);
+        for (uint32_t t = tid; t < (nwords + 3) >> 2; t += bd) {
+          const uint4 v = b4[t];
+          if (v.x | v.y | v.z | v.w) {
+            b4[t] = make_uint4(0, 0, 0, 0);
+            sweep_word(4 * t, v.x);
+            sweep_word(4 * t + 1, v.y);
+            sweep_word(4 * t + 2, v.z);
+            sweep_word(4 * t + 3, v.w);
           }
         }
       }
@@ -622,7 +652,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     // the repeat table's memory held touched words: empty it again
     for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
     __syncthreads();
-    if (tid == 0) atomicAdd(&dbg[7], (unsigned long long)(clock64() - td0));
+    if (prof && tid == 0) atomicAdd(&dbg[7], (unsigned long long)(clock64() - td0));
   }
 }
 
@@ -650,8 +680,9 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
     const long long ts0 = clock64();
-    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg);
-    if (threadIdx.x == 0) {
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
+                a.win_prof);
+    if (a.win_prof && threadIdx.x == 0) {
       const bool tab = a.offU[u + 1] - a.offU[u] <= a.win_pre;
       atomicAdd(tab ? &a.c->prof[0] : &a.c->prof2[0], (unsigned long long)(clock64() - ts0));
       atomicAdd(tab ? &a.c->prof2[2] : &a.c->prof2[1], 1ull);

@@ -323,6 +323,7 @@ struct AggArgs {
   uint64_t win_cap;
   uint32_t win_split;                  // window groups per tier-2 start (>1 for small batches)
   uint32_t win_pre;                    // starts with at most this many lists use precomputed window tables
+  bool win_prof;                       // accumulate tier-2 phase clocks (PBNG_TRACE)
 };
 
 template <int MODE>

@@ -458,14 +458,14 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_vp_agg_win(AggArgs a)
           acc += d;
         }
       };
-      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c->dbg);
+      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c->dbg, false);
       acc = warp_sum(acc);
       if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);
       __syncthreads();
       if (threadIdx.x == 0 && sh.acc) red_add_u64(&a.support[x], sh.acc);
     } else {
       auto out = [&](uint32_t, uint32_t) {};
-      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c->dbg,
+      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c->dbg, false,
                   VpPass2{a.adjV, a.support});
     }
     __syncthreads();

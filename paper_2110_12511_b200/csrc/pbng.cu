@@ -388,6 +388,7 @@ struct State {
   uint64_t win_cap;
   uint32_t win_split = 1;  // window groups per tier-2 start in the next launch
   uint32_t win_pre = 1024;
+  bool prof = std::getenv("PBNG_TRACE") != nullptr;
   // chunked compaction of long lists
   uint2* comp_task;
   uint32_t *comp_tbase, *comp_oldL, *comp_cnt, *comp_ntask;
@@ -508,6 +509,7 @@ AggArgs agg_args(const State& S, int t) {
   a.win_cap = S.win_cap;
   a.win_split = S.win_split;
   a.win_pre = S.win_pre;
+  a.win_prof = S.prof;
   return a;
 }
 
@@ -785,7 +787,11 @@ void fd_grid(Run& r, State& S, const std::vector<uint32_t>& heavy, const std::ve
   unsigned long long* ctl = r.alloc<unsigned long long>(3);
   CK(cudaMemsetAsync(lpos, 0xFF, (size_t)S.g.nU * 4, r.st));
   CK(cudaMemsetAsync(gcnt, 0, (size_t)kGridCnt * 4, r.st));
+  const bool trace = std::getenv("PBNG_TRACE") != nullptr;
   for (uint32_t p : heavy) {
+    cudaEvent_t ta = trace ? r.event() : nullptr;
+    uint32_t rounds = 0;
+    unsigned long long edges = 0;
     const uint32_t n = hcount[p];
     const uint32_t* mem = members + hoff[p];
     const uint32_t maxsel = std::min<uint32_t>(1024, kGridCnt / n);
@@ -802,6 +808,8 @@ void fd_grid(Run& r, State& S, const std::vector<uint32_t>& heavy, const std::ve
       CK(cudaStreamSynchronize(r.st));
       const uint32_t ns = (uint32_t)hc[1];
       if (ns == 0) break;
+      rounds++;
+      edges += hc[2];
       const uint32_t nc = ns * n;
       r.pre(PBNG_K_FD);
       k_fdg_agg<<<r.nsm * 2, kGridThreads, (size_t)nc * 4, r.st>>>(sel, selpre, ns, n, S.g.offU, S.g.adjU, S.g.offV,
@@ -811,6 +819,12 @@ void fd_grid(Run& r, State& S, const std::vector<uint32_t>& heavy, const std::ve
       k_fdg_apply<<<std::max<uint32_t>(1, std::min<uint32_t>((nc + 255) / 256, r.nsm * 4)), 256, 0, r.st>>>(
           nc, n, mem, gcnt, S.support, fdc + 1);
       r.post(PBNG_K_FD);
+    }
+    if (trace) {
+      cudaEvent_t tb = r.event();
+      CK(cudaEventSynchronize(tb));
+      std::fprintf(stderr, "fd-grid part=%u members=%u rounds=%u edges=%llu ms=%.3f\n", p, n, rounds, edges,
+                   elapsed(ta, tb));
     }
   }
 }
