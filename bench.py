@@ -206,16 +206,21 @@ def roofline(stats_list, peaks):
     bytes_alg = 4 * W + 20 * S + 20 * A  # 4 B/wedge, 20 B/(u,v) step, 20 B/update
     achieved = bytes_alg / (agg_ms / 1000) / 1e9 if agg_ms else 0.0
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
+    # DRAM bytes of one captured launch of the dominant kernel (ncu --set full, committed
+    # under profiles/), with that launch's algorithmic bytes beside it
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("agg_dram_bytes_per_wedge")
+            t = json.load(open(tpath))
+            traffic = t["dram_bytes_per_launch"]
+            traffic_note = {k: t[k] for k in ("kernel", "launch", "alg_bytes_per_launch", "dram_over_alg", "source")
+                            if k in t}
         except Exception:
             traffic = None
-    return {"kernel": "wedge aggregation k_agg_{warp,cta,heavy} (count + CD peel)", "bound": "hbm",
+    return {"kernel": "wedge aggregation family: k_agg_warp / k_agg_mid / k_agg_win and the vertex-priority k_vp_agg_* (count + CD peel)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
+            "traffic": traffic, "traffic_launch": traffic_note, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
             else "fallback 6650 GB/s (B200_PROFILING.md)",
             "bytes_alg_per_step": bytes_alg / max(1, len(stats_list)), "agg_ms_per_step": agg_ms / max(1, len(stats_list)),
             "dominant_family_by_time": dominant, "ms_by_family_per_step":

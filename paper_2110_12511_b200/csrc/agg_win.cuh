@@ -64,6 +64,15 @@ constexpr int kDenseDepth = PBNG_DENSE_DEPTH;
 #endif
 constexpr uint32_t kWinChunk = PBNG_WIN_CHUNK ? PBNG_WIN_CHUNK : 512;  // entries per warp task
 
+// bitmap windows with many entries use 256-entry chunks read two 16-byte loads
+// per lane at a time (more bytes in flight); smaller ones 128-entry chunks
+#ifndef PBNG_BIG_WIN
+#define PBNG_BIG_WIN (~0ull)  // off: 256-entry chunks measured no better overall (config 4 worse)
+#endif
+__device__ __forceinline__ uint32_t bitmap_chunk(unsigned long long entries) {
+  return entries >= PBNG_BIG_WIN ? 2 * kWinChunk : kWinChunk;
+}
+
 // chunk size for a window of `entries` entries (PBNG_WIN_CHUNK = 0: about two
 // chunks per warp, 128..1024; else fixed)
 __device__ __forceinline__ uint32_t win_chunk(unsigned long long entries) {
@@ -183,6 +192,7 @@ __device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64
 // id ranges several lanes hit the same word: with PBNG_COMBINE the lanes of a
 // word are grouped (match_any), their bits / increments combined and one lane
 // issues the atomic, instead of the shared-memory unit serialising them.
+template <int D = 1>
 __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, uint32_t a,
                                          uint32_t skip, WinSmem& S, WinShared& sh) {
   const uint32_t ln = lane_id();
@@ -203,7 +213,7 @@ __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_
       if (atomicOr(&S.bits[o >> 5], bit) & bit) win_dup_insert(S, sh, x);
     }
   };
-  seg_visit(p, i0, i1, one);
+  seg_visit<D>(p, i0, i1, one);
 }
 
 // Zero the first nwords words of the window array with 16-byte stores (whole CTA).
@@ -430,8 +440,9 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       // few lists: one warp scans every window's chunk counts (no CTA barriers)
       if (wid == 0) {
         for (uint32_t k = k0; k < k1; k++) {
+          const uint32_t ch = bitmap_chunk(S.ek[k - k0]);
           const uint32_t nch = ln < nl ? (bnd[(uint64_t)ln * W1 + k + 1] - bnd[(uint64_t)ln * W1 + k] +
-                                          kWinChunk - 1) / kWinChunk : 0u;
+                                          ch - 1) / ch : 0u;
           uint32_t incl = nch;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -448,7 +459,8 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       for (uint32_t t0 = 0; t0 < nl; t0 += bd) {
         const uint32_t i = t0 + tid;
         uint32_t nch = 0;
-        if (i < nl) nch = (bnd[(uint64_t)i * W1 + k + 1] - bnd[(uint64_t)i * W1 + k] + kWinChunk - 1) / kWinChunk;
+        const uint32_t ch = bitmap_chunk(S.ek[k - k0]);
+        if (i < nl) nch = (bnd[(uint64_t)i * W1 + k + 1] - bnd[(uint64_t)i * W1 + k] + ch - 1) / ch;
         uint32_t tot;
         const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
         if (i < nl) cpg[(uint64_t)(k - k0) * PL + i] = carry + cp;
@@ -478,6 +490,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       if (insm)
         for (uint32_t i = tid; i < nl; i += bd) S.cpre[i] = cp[i];
       const uint32_t* crow = insm ? S.cpre : cp;
+      const uint32_t wch = bitmap_chunk(S.ek[kr]);
       __syncthreads();
       // warps take chunks dynamically; chunk c belongs to the largest list i with cpre[i] <= c
       auto run = [&](auto&& fn) {
@@ -492,12 +505,15 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
             if (crow[mid] <= c) lo = mid; else hi = mid;
           }
           const uint64_t sbeg = gbase[lo] + bnd[(uint64_t)lo * W1 + k], send = gbase[lo] + bnd[(uint64_t)lo * W1 + k + 1];
-          const uint64_t q0 = sbeg + (uint64_t)(c - crow[lo]) * kWinChunk;
-          fn(q0, q0 + kWinChunk < send ? q0 + kWinChunk : send, e0 + lo);
+          const uint64_t q0 = sbeg + (uint64_t)(c - crow[lo]) * wch;
+          fn(q0, q0 + wch < send ? q0 + wch : send, e0 + lo);
         }
       };
       const long long tm0 = clock64();
-      run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
+      if (wch > kWinChunk)
+        run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<2>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
+      else
+        run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<1>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       __syncthreads();
       const long long tm1 = clock64();
       if (prof && tid == 0) atomicAdd(&dbg[6], (unsigned long long)(tm1 - tm0));

@@ -15,8 +15,17 @@
 namespace pbng {
 
 constexpr uint32_t kFdThreads = 512;
-constexpr uint32_t kFdWarpSlots = 512;
+#ifndef PBNG_FD_WARP_SLOTS
+#define PBNG_FD_WARP_SLOTS 512
+#endif
+#ifndef PBNG_FD_CTA_SLOTS
+#define PBNG_FD_CTA_SLOTS 16384
+#endif
+constexpr uint32_t kFdWarpSlots = PBNG_FD_WARP_SLOTS;  // per-warp table (light vertices)
 constexpr uint32_t kFdWarpCap = kFdWarpSlots / 2;
+constexpr uint32_t kFdCtaSlots = PBNG_FD_CTA_SLOTS;    // CTA table (medium vertices)
+constexpr uint32_t kFdCtaCap = kFdCtaSlots / 2;
+constexpr uint32_t kFdLogCtaSlots = 31 - __builtin_clz(PBNG_FD_CTA_SLOTS);
 constexpr uint64_t kFdWarpWork = 1u << 15;  // wedges above which a vertex goes to the whole CTA
 
 // ---------------------------------------------------------------- membership
@@ -111,7 +120,7 @@ __global__ void k_fd_seg(uint32_t nU, const uint64_t* __restrict__ offU, const u
     if (ln == 0 && acc) {
       atomicAdd(&sw[p], acc);
       const uint64_t d = offU[u + 1] - offU[u];
-      if (acc - d > kCtaCap) atomicAdd(nheavy, 1u);
+      if (acc - d > kFdCtaCap) atomicAdd(nheavy, 1u);
     }
   }
   __syncthreads();
@@ -195,8 +204,8 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   uint32_t* wkeys = sm + w * (2 * kFdWarpSlots);
   uint32_t* wvals = wkeys + kFdWarpSlots;
   uint32_t* ckeys = sm + nw * (2 * kFdWarpSlots);
-  uint32_t* cvals = ckeys + kCtaSlots;
-  uint32_t* s_long = cvals + kCtaSlots;
+  uint32_t* cvals = ckeys + kFdCtaSlots;
+  uint32_t* s_long = cvals + kFdCtaSlots;
   __shared__ uint32_t s_nlong, s_ntouch, s_ndup, s_t, s_nbig, s_n0, s_n1;
   __shared__ unsigned long long s_min;
   __shared__ uint32_t s_hist[65];
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
   __shared__ uint32_t s_scan[33];
   __shared__ FdBand band;
   for (uint32_t i = threadIdx.x; i < nw * 2 * kFdWarpSlots; i += blockDim.x) sm[i] = (i / kFdWarpSlots) % 2 == 0 ? kEmpty : 0u;
-  for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) {
+  for (uint32_t i = threadIdx.x; i < kFdCtaSlots; i += blockDim.x) {
     ckeys[i] = kEmpty;
     cvals[i] = 0;
   }
@@ -488,9 +497,9 @@ __global__ void __launch_bounds__(kFdThreads, 1) k_fd(FdArgs a) {
             }
           }
           __syncthreads();
-        } else if (pb <= kCtaCap) {
+        } else if (pb <= kFdCtaCap) {
           uint32_t logT = ceil_log2(2 * pb);
-          logT = logT > 14 ? 14 : logT;
+          logT = logT > kFdLogCtaSlots ? kFdLogCtaSlots : logT;
           auto f = [&](bool ok, uint32_t x, uint64_t) {
             if (ok && x != u) hash_insert(ckeys, cvals, logT, x);
           };

@@ -54,7 +54,7 @@ size_t range_smem() { return sizeof(RangeSmem); }
 size_t mid_smem() { return sizeof(MidSmem); }
 size_t win_smem() { return sizeof(WinSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
-size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kCtaSlots + kFdThreads) * 4; }
+size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kFdCtaSlots + kFdThreads) * 4; }
 
 void set_attrs_once() {
   static std::once_flag once;
