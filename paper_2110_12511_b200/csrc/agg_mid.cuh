@@ -7,7 +7,14 @@
 #pragma once
 // (included inside namespace pbng by kernels_cd.cuh)
 
-constexpr uint32_t kMidThreads = 512;
+#ifndef PBNG_MID_THREADS
+#define PBNG_MID_THREADS 512
+#endif
+#ifndef PBNG_MID_CTAS
+#define PBNG_MID_CTAS 1
+#endif
+constexpr uint32_t kMidThreads = PBNG_MID_THREADS;
+constexpr uint32_t kMidCtas = PBNG_MID_CTAS;  // resident CTAs per SM
 
 struct MidSmem {
   uint32_t keys[kCtaSlots];
@@ -78,7 +85,7 @@ __device__ __forceinline__ void mid_agg_one(const L& lists, uint64_t e0, uint64_
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kMidThreads, 1) k_agg_mid(AggArgs a) {
+__global__ void __launch_bounds__(kMidThreads, kMidCtas) k_agg_mid(AggArgs a) {
   extern __shared__ __align__(16) unsigned char msm[];
   MidSmem& S = *reinterpret_cast<MidSmem*>(msm);
   __shared__ uint32_t s_nlong, s_t;

@@ -14,9 +14,12 @@ namespace pbng {
 // Per-warp / per-CTA hash capacities (slots are power-of-two; load factor <= 1/2).
 constexpr uint32_t kWarpSlots = 1024;           // tier 0: one warp per u
 constexpr uint32_t kWarpCap = kWarpSlots / 2;   // partners bound for tier 0
-constexpr uint32_t kCtaSlots = 16384;           // tier 1: one CTA per u
-constexpr uint32_t kCtaCap = kCtaSlots / 2;     // partners bound for tier 1
-constexpr uint32_t kLogCtaSlots = 14;
+#ifndef PBNG_MID_LOG_SLOTS
+#define PBNG_MID_LOG_SLOTS 14
+#endif
+constexpr uint32_t kLogCtaSlots = PBNG_MID_LOG_SLOTS;
+constexpr uint32_t kCtaSlots = 1u << kLogCtaSlots;  // tier 1: one CTA per u
+constexpr uint32_t kCtaCap = kCtaSlots / 2;          // partners bound for tier 1
 constexpr uint32_t kWarpTierThreads = 256;
 constexpr uint32_t kHeavyThreads = 512;
 constexpr uint32_t kClassBig = 2048;            // classify: degree handled by a whole CTA

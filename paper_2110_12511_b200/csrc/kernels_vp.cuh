@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kRangeThreads, 1) k_vp_agg_range(AggArgs a) {
 
 // Middle tier: one CTA per start, shared-memory hash table (agg_mid.cuh).
 template <int SIDE>
-__global__ void __launch_bounds__(kMidThreads, 1) k_vp_agg_mid(AggArgs a) {
+__global__ void __launch_bounds__(kMidThreads, kMidCtas) k_vp_agg_mid(AggArgs a) {
   extern __shared__ __align__(16) unsigned char msm[];
   MidSmem& S = *reinterpret_cast<MidSmem*>(msm);
   __shared__ uint32_t s_nlong, s_t;

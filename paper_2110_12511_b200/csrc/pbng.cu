@@ -99,6 +99,22 @@ struct Dev {
   const uint32_t* adjV;
 };
 
+std::vector<cudaEvent_t>& event_pool() {
+  static thread_local std::vector<cudaEvent_t> pool;
+  return pool;
+}
+cudaEvent_t new_event() {
+  std::vector<cudaEvent_t>& pool = event_pool();
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
 class Run {
  public:
   explicit Run(cudaStream_t s) : st(s) {
@@ -111,7 +127,9 @@ class Run {
   ~Run() {
     for (void* p : allocs) cudaFreeAsync(p, st);
     cudaStreamSynchronize(st);
-    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    // events go back to a per-thread pool: creating / destroying thousands of
+    // events per call (one pair per launch with PBNG_OPT_STATS) costs host time
+    for (cudaEvent_t e : events) event_pool().push_back(e);
     if (hc) cudaFreeHost(hc);
     cudaGetLastError();
   }
@@ -129,7 +147,7 @@ class Run {
   }
   cudaEvent_t event() {
     cudaEvent_t e;
-    CK(cudaEventCreate(&e));
+    e = new_event();
     events.push_back(e);
     CK(cudaEventRecord(e, st));
     return e;
@@ -140,7 +158,7 @@ class Run {
     (void)kind;
     pending = nullptr;
     if (timing) {
-      CK(cudaEventCreate(&pending));
+      pending = new_event();
       CK(cudaEventRecord(pending, st));
     }
   }
@@ -149,7 +167,7 @@ class Run {
     launches++;
     if (timing) {
       cudaEvent_t e;
-      CK(cudaEventCreate(&e));
+      e = new_event();
       CK(cudaEventRecord(e, st));
       spans.push_back({kind, pending, e});
       events.push_back(pending);
@@ -523,7 +541,7 @@ void launch_agg(Run& r, const State& S, const uint32_t* ntier) {
   }
   if (ntier[1]) {
     r.pre(PBNG_K_AGG_CTA);
-    k_agg_mid<MODE><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+    k_agg_mid<MODE><<<r.nsm * kMidCtas, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
     r.post(PBNG_K_AGG_CTA);
   }
   if (ntier[2]) {
@@ -567,7 +585,7 @@ void vp_count_live(Run& r, State& S) {
   k_vp_agg_warp<0><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
   r.post(PBNG_K_AGG_WARP);
   r.pre(PBNG_K_AGG_CTA);
-  k_vp_agg_mid<0><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+  k_vp_agg_mid<0><<<r.nsm * kMidCtas, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
   r.post(PBNG_K_AGG_CTA);
   r.pre(PBNG_K_AGG_CTA);
   k_vp_agg_win<0><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
@@ -585,7 +603,7 @@ void vp_count_live(Run& r, State& S) {
   k_vp_agg_warp<1><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
   r.post(PBNG_K_AGG_WARP);
   r.pre(PBNG_K_AGG_CTA);
-  k_vp_agg_mid<1><<<r.nsm, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+  k_vp_agg_mid<1><<<r.nsm * kMidCtas, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
   r.post(PBNG_K_AGG_CTA);
   r.pre(PBNG_K_AGG_CTA);
   k_vp_agg_win<1><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
