@@ -11,7 +11,7 @@
 #define PBNG_MID_THREADS 512
 #endif
 #ifndef PBNG_MID_CTAS
-#define PBNG_MID_CTAS 1
+#define PBNG_MID_CTAS 2
 #endif
 constexpr uint32_t kMidThreads = PBNG_MID_THREADS;
 constexpr uint32_t kMidCtas = PBNG_MID_CTAS;  // resident CTAs per SM

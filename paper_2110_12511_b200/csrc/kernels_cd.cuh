@@ -15,7 +15,7 @@ namespace pbng {
 constexpr uint32_t kWarpSlots = 1024;           // tier 0: one warp per u
 constexpr uint32_t kWarpCap = kWarpSlots / 2;   // partners bound for tier 0
 #ifndef PBNG_MID_LOG_SLOTS
-#define PBNG_MID_LOG_SLOTS 14
+#define PBNG_MID_LOG_SLOTS 13
 #endif
 constexpr uint32_t kLogCtaSlots = PBNG_MID_LOG_SLOTS;
 constexpr uint32_t kCtaSlots = 1u << kLogCtaSlots;  // tier 1: one CTA per u
@@ -194,7 +194,7 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
       if (valid) {
         const uint32_t v = adjU[je + (t - jx)];
         val = ld[v];
-        if (vflag && vflag[v] != epoch) vflag[v] = epoch;
+        if (vflag) atomicAdd(&vflag[v], 1u);  // one more peeled entry in N_v
       }
       // segmented sum over lanes with the same vertex j (contiguous in lane order)
 #pragma unroll
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(512) k_classify_big(const uint2* __restrict__ 
     for (uint64_t k = threadIdx.x; k < d; k += blockDim.x) {
       const uint32_t v = adjU[e0 + k];
       s += ld[v];
-      if (vflag && vflag[v] != epoch) vflag[v] = epoch;
+      if (vflag) atomicAdd(&vflag[v], 1u);
     }
     s = warp_sum(s);
     if (lane_id() == 0) s_part[threadIdx.x >> 5] = s;
@@ -473,15 +473,25 @@ __global__ void __launch_bounds__(256) k_select(uint32_t nU, uint32_t* __restric
 }
 
 // ---------------------------------------------------------------- deletion
-// touched = { v : vflag[v] == epoch } (ballots + block scan, one atomic per tile)
-__global__ void __launch_bounds__(256) k_collect_touched(uint32_t nV, const uint32_t* __restrict__ vflag,
-                                                         uint32_t epoch, uint32_t* __restrict__ touched,
-                                                         Counters* c) {
+// Lazy deletion: vflag[v] counts the entries of N_v peeled since its last
+// compaction.  A list is compacted now when it is short (< big), when at least
+// 1/8 of its live prefix is peeled, or when forced (partition end: FD needs
+// every list grouped by partition).  Stale entries in a live prefix are
+// harmless to the aggregation (peeled partners are filtered when emitting).
+__global__ void __launch_bounds__(256) k_collect_touched(uint32_t nV, uint32_t* __restrict__ vflag,
+                                                         const uint32_t* __restrict__ ld, uint32_t big, bool force,
+                                                         uint32_t* __restrict__ touched, Counters* c) {
   __shared__ uint32_t s_scan[33];
   __shared__ uint32_t s_base;
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < nV; b += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = b + threadIdx.x;
-    const bool t = v < nV && vflag[v] == epoch;
+    const uint32_t dead = v < nV ? vflag[v] : 0u;
+    bool t = dead > 0;
+    if (t && !force) {
+      const uint32_t L = ld[v];
+      t = L < big || (uint64_t)dead * 8 >= L;
+    }
+    if (t) vflag[v] = 0;
     uint32_t total;
     const uint32_t r = block_excl_scan(t ? 1u : 0u, s_scan, &total);
     if (total) {

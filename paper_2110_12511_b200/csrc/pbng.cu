@@ -632,12 +632,13 @@ void count_live(Run& r, State& S) {
   launch_agg<0>(r, S, hc.ntier);
 }
 
-void compact(Run& r, State& S, uint32_t epoch) {
+void compact(Run& r, State& S, uint32_t epoch, bool force = false) {
+  (void)epoch;
   const uint32_t big = kCompChunk;
   CK(cudaMemsetAsync(&S.c->ntouched, 0, 4, r.st));
   CK(cudaMemsetAsync(S.comp_ntask, 0, 4, r.st));
   r.pre(PBNG_K_COMPACT);
-  k_collect_touched<<<r.nsm * 8, 256, 0, r.st>>>(S.g.nV, S.vflag, epoch, S.touched, S.c);
+  k_collect_touched<<<r.nsm * 8, 256, 0, r.st>>>(S.g.nV, S.vflag, S.ld, big, force, S.touched, S.c);
   r.post(PBNG_K_COMPACT);
   r.pre(PBNG_K_COMPACT);
   k_compact<<<r.nsm * 8, 256, 0, r.st>>>(S.touched, &S.c->ntouched, S.g.offV, S.adjL, S.tmp, S.ld, S.part, big,
@@ -777,7 +778,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         rows.push_back(row);
       }
     }
-    if (!del) compact(r, S, epoch);
+    compact(r, S, epoch, true);  // partition end: every list grouped by partition for FD
     scale = part_wc ? (double)first_wc / (double)part_wc : 1.0;
   }
   plan.nparts = (uint32_t)plan.bounds.size() - 1;
