@@ -7,6 +7,16 @@
 #pragma once
 // (included inside namespace pbng by kernels_cd.cuh)
 
+constexpr uint64_t kEmptySlot = 0xFFFFFFFF00000000ull;  // empty (key << 32 | count) slot
+constexpr uint32_t kDupProbe = 32;                     // probe limit of the tier-2 repeat table
+
+// No second pass (CD peel / one-sided count); vertex-priority counting with
+// starts in V supplies VpPass2 (kernels_vp.cuh).
+struct NoPass2 {
+  static constexpr bool kOn = false;
+  __device__ void operator()(uint64_t, unsigned long long) const {}
+};
+
 #ifndef PBNG_MID_THREADS
 #define PBNG_MID_THREADS 512
 #endif

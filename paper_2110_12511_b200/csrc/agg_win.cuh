@@ -1,20 +1,24 @@
 // agg_win.cuh — tier-2 wedge aggregation for starts with more partners than a
-// CTA hash table holds (kCtaCap).  One CTA per start.
+// CTA hash table holds (kCtaCap).  One CTA per start (or per window group of a
+// start when a batch has few starts).
 //
-// Partner ids are processed one id WINDOW at a time (kWindow ids): a shared-
-// memory bitmap records first occurrences (one atomicOr per wedge) and a
-// repeat table counts the partners seen again (w >= 2); after the window the
-// repeats are emitted with w = 1 + repeats (the same window scheme as
-// agg_range.cuh, which replaces the paper's per-thread n-element wedge array,
-// P:388-390).  Lists are sorted, so the part of every list inside a window is
-// one contiguous segment.  The segment bounds of all windows are found once per
-// start (one binary search per list and window, all lanes in parallel) and
-// every window's work is the union of its segments, cut into chunks that all
-// warps share: coalesced 16-byte loads, no per-list cursor traffic.  Starts
-// with more than kWinLists lists search their segments window by window.  If a
-// window's repeats overflow the table it is retried in halves.
+// Partner ids are processed one coarse id WINDOW (kWinIds ids) at a time; this
+// replaces the paper's per-thread n-element wedge array, which on
+// B200 would be an HBM array with one random atomic per wedge.
+//   * sparse window: a shared-memory bitmap records first occurrences (one
+//     atomicOr per wedge) and a repeat table counts the partners seen again;
+//     repeats are emitted with w = 1 + repeats;
+//   * dense window (many entries, or repeats overflowing the table): packed
+//     counters (2..32 bits, the smallest width that holds the start's list
+//     count) over sub-windows; fields with a count >= 2 are emitted.
+// Lists are sorted, so each list's part of a window is one contiguous segment.
+// For starts with up to win_pre lists the segment bounds of every window, the
+// list bases and per-window chunk prefixes are computed once per start into
+// per-CTA scratch; a window's segments are cut into chunks that warps take
+// dynamically (coalesced 16-byte loads).  Starts with more lists search their
+// segments window by window.
 #pragma once
-// (included inside namespace pbng by kernels_cd.cuh, after agg_range.cuh)
+// (included inside namespace pbng by kernels_cd.cuh, after agg_mid.cuh)
 
 #ifndef PBNG_WIN_LOG_IDS
 #define PBNG_WIN_LOG_IDS 20

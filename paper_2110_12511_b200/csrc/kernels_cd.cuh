@@ -23,25 +23,6 @@ constexpr uint32_t kCtaCap = kCtaSlots / 2;          // partners bound for tier 
 constexpr uint32_t kWarpTierThreads = 256;
 constexpr uint32_t kHeavyThreads = 512;
 constexpr uint32_t kClassBig = 2048;            // classify: degree handled by a whole CTA
-// tier 1: range-partitioned CTA hash (see k_agg_range)
-#ifndef PBNG_RANGE_THREADS
-#define PBNG_RANGE_THREADS 1024
-#endif
-#ifndef PBNG_RANGE_SLOTS
-#define PBNG_RANGE_SLOTS 16384
-#endif
-#ifndef PBNG_RANGE_CTAS
-#define PBNG_RANGE_CTAS 1
-#endif
-#ifndef PBNG_PIECE
-#define PBNG_PIECE 512
-#endif
-constexpr uint32_t kRangeThreads = PBNG_RANGE_THREADS;
-constexpr uint32_t kRangeSlots = PBNG_RANGE_SLOTS;  // table slots; at most half are filled per range
-constexpr uint32_t kRangeCtas = PBNG_RANGE_CTAS;    // resident CTAs per SM (overlap barrier waits)
-constexpr uint32_t kRangeLogSlots = 31 - __builtin_clz(PBNG_RANGE_SLOTS);
-constexpr uint32_t kPiece = PBNG_PIECE;             // partner lists are walked in pieces of this length
-
 // Range histogram: 16-bit-style log-scale keys of the 64-bit support
 // (exact below 256; 8 mantissa bits above), weighted by the static wedge work.
 constexpr uint32_t kBins = 14336;
@@ -101,35 +82,30 @@ __global__ void k_init_v(uint32_t nV, const uint64_t* __restrict__ offV, uint32_
   if (lane_id() == 0 && acc) atomicAdd(sum_d2, acc);
 }
 
-// wc[u] = Σ_{v ∈ N_u} d_v : static wedge work of peeling u (proxy 2; g5)
-// Also the most list pieces any u can have (tier-1 cursor scratch size).
+// wc[u] = Σ_{v ∈ N_u} d_v : static wedge work of peeling u (proxy 2; g5),
+// and ∧_cnt = Σ_(u,v) min(d_u, d_v), the re-count cost.
 __global__ void k_init_u(uint32_t nU, const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                          const uint64_t* __restrict__ offV, uint64_t* __restrict__ wc,
-                         uint32_t* __restrict__ part, unsigned long long* max_pieces,
-                         unsigned long long* sum_min) {
+                         uint32_t* __restrict__ part, unsigned long long* sum_min) {
   const uint32_t ln = lane_id();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long mp = 0, smin = 0;
+  unsigned long long smin = 0;
   for (uint64_t u = gw; u < nU; u += nw) {
-    uint64_t s = 0, pc = 0;
+    uint64_t s = 0;
     const uint64_t du = offU[u + 1] - offU[u];
     for (uint64_t e = offU[u] + ln; e < offU[u + 1]; e += 32) {
       uint32_t v = adjU[e];
       const uint64_t d = offV[v + 1] - offV[v];
       s += d;
-      pc += (d + kPiece - 1) / kPiece;
       smin += d < du ? d : du;
     }
     s = warp_sum(s);
-    pc = warp_sum(pc);
-    mp = pc > mp ? pc : mp;
     if (ln == 0) {
       wc[u] = s;
       part[u] = kUnassigned;
     }
   }
-  if (ln == 0 && mp) atomicMax(max_pieces, mp);
   smin = warp_sum(smin);
   if (ln == 0 && smin) atomicAdd(sum_min, smin);
 }
@@ -309,16 +285,9 @@ struct AggArgs {
   const uint2* __restrict__ list;
   const uint32_t* __restrict__ count;
   uint32_t nU;
-  uint32_t* ticket;      // dynamic scheduling counter (tier 1)
-  uint64_t* piece_pos;   // tier 1 per-CTA piece cursors (piece_cap per CTA)
-  uint64_t* piece_end;
-  uint64_t* piece_save;
-  uint32_t* piece_head;
-  uint32_t* piece_srange;
-  uint64_t piece_cap;
+  uint32_t* ticket;      // dynamic scheduling counter (tiers 1-2)
   Counters* c;
   // vertex-priority counting (kernels_vp.cuh)
-  uint64_t* piece_pedge;               // tier 1: list (edge index) of each piece (pass 2)
   const uint32_t* __restrict__ cutV;   // per v: live entries of N_v ranked above v (Alg.1 l.10)
   const uint32_t* __restrict__ cutU;   // per u: entries of N_u ranked above u
   // tier 2 (agg_win.cuh): per-CTA window-bound scratch
@@ -393,7 +362,6 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
   }
 }
 
-#include "agg_range.cuh"
 #include "agg_mid.cuh"
 #include "agg_win.cuh"
 

@@ -79,25 +79,6 @@ __global__ void k_vp_cut_u(uint32_t nU, const uint64_t* __restrict__ offU, const
   }
 }
 
-// most list pieces any V start can have (tier-1 cursor scratch size)
-__global__ void k_vp_vpieces(uint32_t nV, const uint64_t* __restrict__ offV, const uint32_t* __restrict__ adjV,
-                             const uint64_t* __restrict__ offU, unsigned long long* max_pieces) {
-  const uint32_t ln = lane_id();
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long mp = 0;
-  for (uint64_t v = gw; v < nV; v += nw) {
-    uint64_t pc = 0;
-    for (uint64_t e = offV[v] + ln; e < offV[v + 1]; e += 32) {
-      const uint32_t u = adjV[e];
-      pc += (offU[u + 1] - offU[u] + kPiece - 1) / kPiece;
-    }
-    pc = warp_sum(pc);
-    mp = pc > mp ? pc : mp;
-  }
-  if (ln == 0 && mp) atomicMax(max_pieces, mp);
-}
-
 // Edge range of a start and its partner-list source.
 template <int SIDE>
 struct VpSide;
@@ -328,53 +309,6 @@ struct VpPass2 {
     red_add_u64(&support[adjL[e]], cs);
   }
 };
-
-// Tier 1: one CTA per start, range-partitioned bitmap + repeat table
-// (agg_range.cuh) over the id space [0, start) — lasts ranked above the start.
-template <int SIDE>
-__global__ void __launch_bounds__(kRangeThreads, 1) k_vp_agg_range(AggArgs a) {
-  extern __shared__ __align__(16) unsigned char rsm[];
-  RangeSmem& S = *reinterpret_cast<RangeSmem*>(rsm);
-  __shared__ RangeShared sh;
-  for (uint32_t i = threadIdx.x; i < kBitWords; i += blockDim.x) S.bits[i] = 0;
-  for (uint32_t i = threadIdx.x; i < kDupSlots; i += blockDim.x) S.dup[i] = kEmptySlot;
-  const uint64_t cap = a.piece_cap;
-  const Pieces pc{a.piece_pos + blockIdx.x * cap,    a.piece_end + blockIdx.x * cap,
-                  a.piece_save + blockIdx.x * cap,   a.piece_head + blockIdx.x * cap,
-                  a.piece_srange + blockIdx.x * cap, a.piece_pedge + blockIdx.x * cap};
-  const uint32_t n = *a.count;
-  const auto L = VpSide<SIDE>::lists(a);
-  const uint32_t* __restrict__ partner = VpSide<SIDE>::partners(a);
-  for (;;) {
-    if (threadIdx.x == 0) sh.t = atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    const uint32_t i = sh.t;
-    if (threadIdx.x == 0) sh.acc = 0;
-    __syncthreads();
-    if (i >= n) break;
-    const uint32_t x = a.list[i].x;
-    uint64_t e0, e1;
-    VpSide<SIDE>::range(a, x, e0, e1);
-    if (SIDE == 0) {
-      uint64_t acc = 0;
-      auto out = [&](uint32_t k, uint32_t wv) {
-        if (a.part[k] == kUnassigned) {
-          const uint64_t d = choose2(wv);
-          red_add_u64(&a.support[k], d);
-          acc += d;
-        }
-      };
-      range_agg_one(L, e0, e1, 0xFFFFFFFFu, x, partner, S, pc, sh, out, a.c->dbg);
-      acc = warp_sum(acc);
-      if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);
-      __syncthreads();
-      if (threadIdx.x == 0 && sh.acc) red_add_u64(&a.support[x], sh.acc);
-    } else {
-      auto out = [&](uint32_t, uint32_t) {};
-      range_agg_one(L, e0, e1, 0xFFFFFFFFu, x, partner, S, pc, sh, out, a.c->dbg, VpPass2{a.adjV, a.support});
-    }
-  }
-}
 
 // Middle tier: one CTA per start, shared-memory hash table (agg_mid.cuh).
 template <int SIDE>

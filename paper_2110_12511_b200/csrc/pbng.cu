@@ -50,7 +50,6 @@ void check(cudaError_t e, const char* what, int line) {
 constexpr uint64_t kInf = ~0ull;
 
 size_t warp_tier_smem() { return (size_t)(kWarpTierThreads / 32) * 2 * kWarpSlots * 4; }
-size_t range_smem() { return sizeof(RangeSmem); }
 size_t mid_smem() { return sizeof(MidSmem); }
 size_t win_smem() { return sizeof(WinSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
@@ -68,8 +67,6 @@ void set_attrs_once() {
     }
     cudaFuncSetAttribute(k_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
-    cudaFuncSetAttribute(k_agg_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
-    cudaFuncSetAttribute(k_agg_range<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
     cudaFuncSetAttribute(k_agg_mid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
     cudaFuncSetAttribute(k_agg_mid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
     cudaFuncSetAttribute(k_vp_agg_mid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
@@ -80,8 +77,6 @@ void set_attrs_once() {
     cudaFuncSetAttribute(k_vp_agg_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_vp_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
-    cudaFuncSetAttribute(k_vp_agg_range<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
-    cudaFuncSetAttribute(k_vp_agg_range<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)range_smem());
     cudaFuncSetAttribute(k_range_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem());
     cudaFuncSetAttribute(k_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem());
     cudaFuncSetAttribute(k_fdg_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kGridCnt * 4));
@@ -397,11 +392,6 @@ struct State {
   unsigned long long* sum_d2;
   uint32_t nslots;
   uint32_t *slot_cnt, *slot_touch, *slot_dup;  // FD heavy path: dense counters per CTA
-  uint64_t piece_cap;                          // tier-1 cursor scratch per CTA
-  uint64_t *piece_pos, *piece_end, *piece_save;
-  uint32_t* piece_head;
-  uint32_t* piece_srange;
-  uint64_t* piece_pedge;
   uint32_t* win_bnd;  // tier-2 window bounds, win_cap per CTA
   uint64_t win_cap;
   uint32_t win_split = 1;  // window groups per tier-2 start in the next launch
@@ -465,10 +455,8 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank&
   r.pre(PBNG_K_INIT);
   k_init_v<<<r.nsm * 4, 256, 0, r.st>>>(g.nV, g.offV, S.ld, S.sum_d2);
   r.post(PBNG_K_INIT);
-  unsigned long long* dmax = r.alloc<unsigned long long>(1);
-  CK(cudaMemsetAsync(dmax, 0, 8, r.st));
   r.pre(PBNG_K_INIT);
-  k_init_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, g.offV, S.wc, S.part, dmax, S.sum_min);
+  k_init_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, g.offV, S.wc, S.part, S.sum_min);
   r.post(PBNG_K_INIT);
   S.cutU = S.cutV = nullptr;
   if (vp) {
@@ -477,21 +465,7 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank&
     r.pre(PBNG_K_COUNT_VP);
     k_vp_cut_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, RV.binoff, RV.dmax, S.cutU);
     r.post(PBNG_K_COUNT_VP);
-    r.pre(PBNG_K_COUNT_VP);
-    k_vp_vpieces<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, g.offV, g.adjV, g.offU, dmax);
-    r.post(PBNG_K_COUNT_VP);
   }
-  unsigned long long hmax = 0;
-  CK(cudaMemcpyAsync(&hmax, dmax, 8, cudaMemcpyDeviceToHost, r.st));
-  CK(cudaStreamSynchronize(r.st));
-  S.piece_cap = std::max<unsigned long long>(hmax, 1);
-  const size_t np = (size_t)r.nsm * kRangeCtas * S.piece_cap;
-  S.piece_pos = r.alloc<uint64_t>(np);
-  S.piece_end = r.alloc<uint64_t>(np);
-  S.piece_save = r.alloc<uint64_t>(np);
-  S.piece_head = r.alloc<uint32_t>(np);
-  S.piece_srange = r.alloc<uint32_t>(np);
-  S.piece_pedge = vp ? r.alloc<uint64_t>(np) : nullptr;
   const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWinIds - 1) / kWinIds;
   // per-CTA tables of starts with up to win_pre lists: bounds + chunk prefixes
   // ((W+1) u32 each per list) and list bases (u64); about 8 MB per CTA at most
@@ -513,14 +487,7 @@ AggArgs agg_args(const State& S, int t) {
   a.count = &S.c->ntier[t];
   a.nU = S.g.nU;
   a.ticket = &S.c->ticket[t];
-  a.piece_pos = S.piece_pos;
-  a.piece_end = S.piece_end;
-  a.piece_save = S.piece_save;
-  a.piece_head = S.piece_head;
-  a.piece_srange = S.piece_srange;
-  a.piece_cap = S.piece_cap;
   a.c = S.c;
-  a.piece_pedge = S.piece_pedge;
   a.cutV = S.cutV;
   a.cutU = S.cutU;
   a.win_bnd = S.win_bnd;
