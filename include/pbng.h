@@ -112,8 +112,10 @@ enum {
   PBNG_OPT_FORCE_RECOUNT = 16, /* test hook: take the re-count branch every CD iteration */
   PBNG_OPT_ONESIDED_COUNT = 32, /* count (and re-count) by one-sided wedge aggregation, W = Σ_v d_v^2
                                    (P:369-373), instead of vertex-priority counting (Alg.1) */
-  PBNG_OPT_FD_GRID = 64         /* test hook: peel every FD partition of <= 4096 members on the whole GPU
+  PBNG_OPT_FD_GRID = 64,        /* test hook: peel every FD partition of <= 4096 members on the whole GPU
                                    (by default only partitions with far above average work) */
+  PBNG_OPT_STATS_DEFER = 128    /* like PBNG_OPT_STATS, but the per-kernel-family device times are
+                                   summed later by pbng_kernel_times() instead of inside the call */
 };
 
 /* Per-vertex butterfly counts of the peel side:
@@ -153,6 +155,14 @@ int pbng_tip_decompose_host(pbng_csr U, pbng_csr V, int side, uint32_t P, uint64
  *   out_nparts   HOST pointer, partitions produced. */
 int pbng_tip_plan(pbng_csr U, pbng_csr V, int side, uint32_t P, uint32_t opts, uint32_t* out_part,
                   uint64_t* out_init, uint64_t* out_bounds, uint32_t* out_nparts, void* stream);
+
+/* Device time per kernel family (ms, indexed by PBNG_K_*) of the last call on
+ * this thread made with PBNG_OPT_STATS_DEFER: the call only records a CUDA
+ * event pair around each launch on its stream; this function waits for and
+ * sums them, so a caller timing the call itself does not pay for the queries.
+ * out_ms: host array of PBNG_K_NUM floats.  Returns PBNG_ERR_ARG if out_ms is
+ * NULL; all zeros if no deferred call was made since the last query. */
+int pbng_kernel_times(float* out_ms);
 
 /* Message for the last non-OK return on this thread ("" if none). */
 const char* pbng_last_error(void);

@@ -28,12 +28,12 @@ LIB_PATH = os.environ.get("PBNG_LIB") or os.path.join(_HERE, "libpbng.so")
 
 OK, ERR_ARG, ERR_GRAPH, ERR_OOM, ERR_CUDA = 0, 1, 2, 3, 4
 OPT_NO_RECOUNT, OPT_NO_DELETE, OPT_VALIDATE, OPT_STATS, OPT_FORCE_RECOUNT, OPT_ONESIDED_COUNT = 1, 2, 4, 8, 16, 32
-OPT_FD_GRID = 64
+OPT_FD_GRID, OPT_STATS_DEFER = 64, 128
 MAX_P = 4096
 KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_heavy", "select", "range", "compact",
                    "fd_build", "fd", "count_vp")
 EXPORTS = ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
-           "pbng_last_error", "pbng_version")
+           "pbng_kernel_times", "pbng_last_error", "pbng_version")
 
 
 class PbngError(RuntimeError):
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         for f in ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan"):
             getattr(lib, f).restype = ctypes.c_int
+        lib.pbng_kernel_times.argtypes = [ctypes.c_void_p]
+        lib.pbng_kernel_times.restype = ctypes.c_int
         lib.pbng_last_error.restype = ctypes.c_char_p
         lib.pbng_last_error.argtypes = []
         lib.pbng_version.restype = ctypes.c_char_p
@@ -203,11 +205,19 @@ def pbng_tip_decompose_host(off_u, adj_u, off_v, adj_v, P: int, side: int = 0, o
     return out, st.as_dict()
 
 
+def pbng_kernel_times() -> dict:
+    """Device ms per kernel family of the last call made with OPT_STATS_DEFER."""
+    out = (ctypes.c_float * 16)()
+    _check(load_library().pbng_kernel_times(ctypes.cast(out, ctypes.c_void_p)))
+    return {name: round(float(out[i]), 4) for i, name in enumerate(KERNEL_FAMILIES) if out[i]}
+
+
 def as_u64(t) -> np.ndarray:
     """Device int64 tensor of uint64 bits -> numpy uint64."""
     return t.cpu().numpy().view(np.uint64)
 
 
+kernel_times = pbng_kernel_times
 count_butterflies = pbng_count_butterflies
 tip_decompose = pbng_tip_decompose
 tip_plan = pbng_tip_plan

@@ -110,6 +110,17 @@ cudaEvent_t new_event() {
   return e;
 }
 
+// Per-launch event pairs of the last call made with PBNG_OPT_STATS_DEFER,
+// summed by pbng_kernel_times() (so the queries run after the caller's timing).
+struct DeferredSpan {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::vector<DeferredSpan>& deferred_spans() {
+  static thread_local std::vector<DeferredSpan> spans;
+  return spans;
+}
+
 class Run {
  public:
   explicit Run(cudaStream_t s) : st(s) {
@@ -123,8 +134,17 @@ class Run {
     for (void* p : allocs) cudaFreeAsync(p, st);
     cudaStreamSynchronize(st);
     // events go back to a per-thread pool: creating / destroying thousands of
-    // events per call (one pair per launch with PBNG_OPT_STATS) costs host time
+    // events per call (one pair per launch with PBNG_OPT_STATS) costs host time;
+    // with deferral the span events are kept for pbng_kernel_times()
     for (cudaEvent_t e : events) event_pool().push_back(e);
+    for (const Span& sp : spans) {
+      if (defer) {
+        deferred_spans().push_back({sp.kind, sp.a, sp.b});
+      } else {
+        event_pool().push_back(sp.a);
+        event_pool().push_back(sp.b);
+      }
+    }
     if (hc) cudaFreeHost(hc);
     cudaGetLastError();
   }
@@ -164,9 +184,7 @@ class Run {
       cudaEvent_t e;
       e = new_event();
       CK(cudaEventRecord(e, st));
-      spans.push_back({kind, pending, e});
-      events.push_back(pending);
-      events.push_back(e);
+      spans.push_back({kind, pending, e});  // span events live in `spans` only
     }
   }
   void kernel_ms(float* out) {
@@ -181,6 +199,7 @@ class Run {
   int nsm = 148;
   Counters* hc = nullptr;
   bool timing = false;
+  bool defer = false;
   uint32_t launches = 0;
 
  private:
@@ -980,7 +999,15 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   pbng_stats st;
   std::memset(&st, 0, sizeof(st));
   Run r(s);
-  r.timing = (opts & PBNG_OPT_STATS) != 0;
+  r.timing = (opts & (PBNG_OPT_STATS | PBNG_OPT_STATS_DEFER)) != 0;
+  r.defer = (opts & PBNG_OPT_STATS_DEFER) != 0;
+  if (r.defer) {  // a new deferred call replaces the previous one's spans
+    for (const DeferredSpan& sp : deferred_spans()) {
+      event_pool().push_back(sp.a);
+      event_pool().push_back(sp.b);
+    }
+    deferred_spans().clear();
+  }
   if (opts & PBNG_OPT_VALIDATE) validate(r, g);
   if (g.nU == 0) {
     if (out.bounds) {
@@ -1033,7 +1060,7 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   }
   CK(cudaStreamSynchronize(r.st));
   st.launches = r.launches;
-  if (r.timing) r.kernel_ms(st.ms_kernel);
+  if (r.timing && !r.defer) r.kernel_ms(st.ms_kernel);
   if (stats) *stats = st;
 }
 
@@ -1133,6 +1160,22 @@ int pbng_tip_decompose_host(pbng_csr U, pbng_csr V, int side, uint32_t P, uint64
     decompose(g, P, opts, o, stats, s);
     if (nOut) CK(cudaMemcpyAsync(out_tip, dtip, (size_t)nOut * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+  });
+}
+
+int pbng_kernel_times(float* out_ms) {
+  return guarded([&] {
+    if (!out_ms) fail(PBNG_ERR_ARG, "out_ms is null");
+    for (int i = 0; i < PBNG_K_NUM; i++) out_ms[i] = 0.0f;
+    for (const DeferredSpan& sp : deferred_spans()) {
+      float ms = 0;
+      CK(cudaEventSynchronize(sp.b));
+      CK(cudaEventElapsedTime(&ms, sp.a, sp.b));
+      out_ms[sp.kind] += ms;
+      event_pool().push_back(sp.a);
+      event_pool().push_back(sp.b);
+    }
+    deferred_spans().clear();
   });
 }
 

@@ -290,3 +290,17 @@ def test_fd_grid_path_configs(pb, cfg):
     want = _config3_theta(g) if cfg == 3 else oracle.bup_tip(g)
     tip, st = pb.pbng_tip_decompose(dev(pb, g), 400 if cfg == 3 else P, opts=pb.OPT_FD_GRID)
     assert np.array_equal(pb.as_u64(tip), want)
+
+
+def test_kernel_times_deferred(pb):
+    """PBNG_OPT_STATS_DEFER: the call records per-launch events, pbng_kernel_times sums them."""
+    g, P = gg.config(1)
+    d = dev(pb, g)
+    tip, st = pb.pbng_tip_decompose(d, P, opts=pb.OPT_STATS_DEFER)
+    assert np.array_equal(pb.as_u64(tip), oracle.bup_tip(g))
+    assert st["ms_kernel"] == {}
+    kt = pb.pbng_kernel_times()
+    assert kt and all(v >= 0 for v in kt.values()) and "fd" in kt
+    assert pb.pbng_kernel_times() == {}  # consumed
+    _, st2 = pb.pbng_tip_decompose(d, P, opts=pb.OPT_STATS)
+    assert set(st2["ms_kernel"]) == set(kt)
