@@ -207,18 +207,35 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
     warp_append2(tier == 2, item, tier2, &c->ntier[2]);
     __syncwarp();
   }
+  // counters: warp sums, then one set of atomics per CTA (all of them hit one
+  // cache line, so per-warp atomics from every warp would serialise in L2)
+  __shared__ unsigned long long s_red[5][8];
   wsum = warp_sum(wsum);
   ssum = warp_sum(ssum);
   tw[0] = warp_sum(tw[0]);
   tw[1] = warp_sum(tw[1]);
   tw[2] = warp_sum(tw[2]);
-  if (ln == 0 && wsum) {
-    atomicAdd(&c->wedges, wsum);
-    atomicAdd(&c->cum_wedges, wsum);
-    atomicAdd(&c->cum_steps, ssum);
-    if (tw[0]) atomicAdd(&c->tier_wedges[0], tw[0]);
-    if (tw[1]) atomicAdd(&c->tier_wedges[1], tw[1]);
-    if (tw[2]) atomicAdd(&c->tier_wedges[2], tw[2]);
+  if (ln == 0) {
+    s_red[0][wib] = wsum;
+    s_red[1][wib] = ssum;
+    s_red[2][wib] = tw[0];
+    s_red[3][wib] = tw[1];
+    s_red[4][wib] = tw[2];
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    unsigned long long s = 0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); w++) s += s_red[threadIdx.x][w];
+    if (s) {
+      if (threadIdx.x == 0) {
+        atomicAdd(&c->wedges, s);
+        atomicAdd(&c->cum_wedges, s);
+      } else if (threadIdx.x == 1) {
+        atomicAdd(&c->cum_steps, s);
+      } else {
+        atomicAdd(&c->tier_wedges[threadIdx.x - 2], s);
+      }
+    }
   }
 }
 
@@ -436,8 +453,15 @@ __global__ void __launch_bounds__(256) k_select(uint32_t nU, uint32_t* __restric
       __syncthreads();
     }
   }
+  __shared__ unsigned long long s_red[8];  // launched with 256 threads: one atomic per CTA
   swc = warp_sum(swc);
-  if (lane_id() == 0 && swc) atomicAdd(&c->sel_wc, swc);
+  if (lane_id() == 0) s_red[threadIdx.x >> 5] = swc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); w++) s += s_red[w];
+    if (s) atomicAdd(&c->sel_wc, s);
+  }
 }
 
 // ---------------------------------------------------------------- deletion
