@@ -156,6 +156,26 @@ int pbng_tip_decompose_host(pbng_csr U, pbng_csr V, int side, uint32_t P, uint64
 int pbng_tip_plan(pbng_csr U, pbng_csr V, int side, uint32_t P, uint32_t opts, uint32_t* out_part,
                   uint64_t* out_init, uint64_t* out_bounds, uint32_t* out_nparts, void* stream);
 
+/* One level of the k-tip hierarchy, retrieved from tip numbers (P:463-475:
+ * tip numbers index "any level of the k-tip hierarchy"; k-tip = Def. 2,
+ * P:451-459).  The level is the subgraph induced on U_k = {u : tip[u] >= k}
+ * and all of V; its k-tips are the classes of U_k under butterfly
+ * connectivity (u ~ u' iff |N_u ∩ N_u'| >= 2, i.e. they share a butterfly,
+ * closed transitively: "connected by a series of butterflies").
+ *   tip        device, peel-side n entries (normally pbng_tip_decompose's
+ *              output; any uint64 vector is accepted and defines U_k).
+ *   k          the level; k = 0 keeps every u (vertices in no butterfly are
+ *              singleton components); k > max θ gives an empty level.
+ *   out_comp   device, peel-side n entries: the smallest id (caller labels)
+ *              of u's k-tip, or 0xFFFFFFFF when tip[u] < k.  Labels are
+ *              canonical, so results compare bit-exactly.
+ *   out_ncomp  HOST pointer: number of k-tips (components) in the level.
+ * Computed by the one-sided aggregation tiers (LINK mode: union-find over
+ * pairs with w >= 2) on the level's subgraph.  Errors as above; PBNG_ERR_ARG
+ * for null pointers. */
+int pbng_tip_components(pbng_csr U, pbng_csr V, int side, const uint64_t* tip, uint64_t k, uint32_t* out_comp,
+                        uint32_t* out_ncomp, void* stream);
+
 /* Device time per kernel family (ms, indexed by PBNG_K_*) of the last call on
  * this thread made with PBNG_OPT_STATS_DEFER: the call only records a CUDA
  * event pair around each launch on its stream; this function waits for and

@@ -8,6 +8,8 @@ the paper.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
   count(g)            -> uint64 support per u    (oracle.c: oracle_count)
   count_subset(g, us) -> uint64 support per listed u
   bup_tip(g)          -> uint64 tip number per u (oracle.c: oracle_bup_tip)
+  tip_level(g, θ, k)  -> (uint32 k-tip label per u, number of k-tips)
+                         (oracle.c: oracle_tip_level, P:451-475)
   brute.*             pure-Python brute force and Definition-2 tip numbers for
                       tiny graphs (oracle/brute.py)
 
@@ -60,6 +62,8 @@ def _load():
         _lib.oracle_bup_tip.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
         for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip):
             f.restype = ctypes.c_int
+        _lib.oracle_tip_level.argtypes = base + [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+        _lib.oracle_tip_level.restype = ctypes.c_int64
         _lib.oracle_cert_support_ge.argtypes = base + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                                        ctypes.c_void_p]
         _lib.oracle_cert_support_ge.restype = ctypes.c_int
@@ -107,6 +111,19 @@ def bup_tip(g, stats: Stats | None = None) -> np.ndarray:
         raise MemoryError("oracle_bup_tip failed")
     del keep
     return out
+
+
+def tip_level(g, theta, k: int):
+    """k-tips of level k (Def. 2; retrieval from θ):
+    (label per u = smallest id of its k-tip or 0xFFFFFFFF when θ_u < k, number of k-tips)."""
+    keep, ptrs = _csr(g)
+    th = np.ascontiguousarray(theta, np.uint64)
+    out = np.zeros(g.nU, np.uint32)
+    n = _load().oracle_tip_level(g.nU, g.nV, *ptrs, th.ctypes.data, int(k), out.ctypes.data)
+    if n < 0:
+        raise MemoryError("oracle_tip_level failed")
+    del keep
+    return out, int(n)
 
 
 def cert_support_ge(g, theta, us=None) -> np.ndarray:

@@ -10,6 +10,11 @@ plain definitions the paper states, written out with no algorithmic shortcut:
                         butterflies of H (Definition 2, tip number
                         P:469-471).  Every k in [0, max support] is swept
                         (tip numbers can fall between initial supports).
+  k_tips(g, k)          the k-tips of Definition 2 straight from the
+                        4-tuples, without tip numbers: the largest vertex set
+                        in which every u has >= k butterflies (iterated
+                        removal), split into classes of "connected by a
+                        series of butterflies"; label = smallest id.
   init_support(g, part) butterflies u shares only with vertices of partitions
                         j >= part[u] (the support initialisation vector,
                         P:781-786), counted from the 4-tuples.
@@ -78,3 +83,28 @@ def init_support(g, part):
         if part[u] >= part[u2]:
             s[u2] += 1
     return s
+
+
+def k_tips(g, k):
+    """(label per u — smallest id of its k-tip, or 0xFFFFFFFF outside every k-tip —, number of k-tips)."""
+    _, _, _, tuples = butterflies(g)
+    members = set(range(g.nU))
+    while True:
+        s = _support_within(tuples, members)
+        drop = {u for u in members if s[u] < k}
+        if not drop:
+            break
+        members -= drop
+    # butterfly connectivity inside the member set: merge classes per butterfly
+    cls = {u: {u} for u in members}
+    for (u, u2, _, _) in tuples:
+        if u in members and u2 in members and cls[u] is not cls[u2]:
+            merged = cls[u] | cls[u2]
+            for x in merged:
+                cls[x] = merged
+    label = [0xFFFFFFFF] * g.nU
+    roots = set()
+    for u in members:
+        label[u] = min(cls[u])
+        roots.add(label[u])
+    return label, len(roots)

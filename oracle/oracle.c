@@ -21,6 +21,13 @@
  *                    Alg.2 l.11 P:526 / S:259; tie-break lowest id, reading g2).
  *   oracle_count_subset  oracle_count restricted to a list of u (for sampled
  *                    checks at sizes where the full oracle is too slow).
+ *   oracle_tip_level one level of the k-tip hierarchy from tip numbers
+ *                    (k-tip = Def. 2): members
+ *                    U_k = {theta >= k}, V(H) = V; two members are adjacent
+ *                    when they share a butterfly (|N_u ∩ N_u'| >= 2); the
+ *                    k-tips are the connected components of that relation
+ *                    ("connected by a series of butterflies"), found by
+ *                    breadth-first search; label = smallest member id.
  *
  * Pins (tests/test_oracle.py, -m "not gpu"): brute-force 4-tuple enumeration,
  * K_{a,b} closed form, sum_U = sum_V identity, tip numbers by Definition 2
@@ -190,4 +197,54 @@ int oracle_bup_tip(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_
   if (st) { st->wedges += local.wedges; st->updates += local.updates; st->peeled += local.peeled; }
   free(support); free(alive); free(cnt); free(touched); free(h.heap); free(h.pos);
   return 0;
+}
+
+/* comp[u] = smallest id of u's k-tip if theta[u] >= k, else 0xFFFFFFFF;
+ * returns the number of k-tips (or -1 on allocation failure).  Plain BFS over
+ * members; the neighbours of a member are the members it shares >= 2
+ * neighbours with, found by the same dense counter array as oracle_count.
+ * Members are visited in increasing id, so each BFS root is the smallest id
+ * of its component. */
+int64_t oracle_tip_level(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
+                         const uint64_t* offV, const uint32_t* adjV, const uint64_t* theta, uint64_t k,
+                         uint32_t* comp) {
+  (void)nV;
+  size_t n1 = nU ? nU : 1;
+  uint32_t* cnt = (uint32_t*)calloc(n1, sizeof(uint32_t));
+  uint32_t* touched = (uint32_t*)malloc(n1 * sizeof(uint32_t));
+  uint32_t* queue = (uint32_t*)malloc(n1 * sizeof(uint32_t));
+  if (!cnt || !touched || !queue) { free(cnt); free(touched); free(queue); return -1; }
+  for (uint32_t u = 0; u < nU; u++) comp[u] = 0xFFFFFFFFu;
+  int64_t ncomp = 0;
+  for (uint32_t root = 0; root < nU; root++) {
+    if (theta[root] < k || comp[root] != 0xFFFFFFFFu) continue;
+    ncomp++;
+    uint64_t head = 0, tail = 0;
+    comp[root] = root;
+    queue[tail++] = root;
+    while (head < tail) {
+      uint32_t u = queue[head++];
+      uint64_t nt = 0;
+      for (uint64_t e = offU[u]; e < offU[u + 1]; e++) {
+        uint32_t v = adjU[e];
+        for (uint64_t f = offV[v]; f < offV[v + 1]; f++) {
+          uint32_t u2 = adjV[f];
+          if (u2 == u || theta[u2] < k) continue;
+          if (cnt[u2]++ == 0) touched[nt++] = u2;
+        }
+      }
+      for (uint64_t t = 0; t < nt; t++) {
+        uint32_t u2 = touched[t];
+        if (cnt[u2] >= 2 && comp[u2] == 0xFFFFFFFFu) {
+          comp[u2] = root;
+          queue[tail++] = u2;
+        }
+        cnt[u2] = 0;
+      }
+    }
+  }
+  free(cnt);
+  free(touched);
+  free(queue);
+  return ncomp;
 }

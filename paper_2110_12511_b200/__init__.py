@@ -33,7 +33,7 @@ MAX_P = 4096
 KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_heavy", "select", "range", "compact",
                    "fd_build", "fd", "count_vp")
 EXPORTS = ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
-           "pbng_kernel_times", "pbng_last_error", "pbng_version")
+           "pbng_tip_components", "pbng_kernel_times", "pbng_last_error", "pbng_version")
 
 
 class PbngError(RuntimeError):
@@ -82,7 +82,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pbng_tip_decompose_host.argtypes = lib.pbng_tip_decompose.argtypes
         lib.pbng_tip_plan.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
-        for f in ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan"):
+        lib.pbng_tip_components.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        for f in ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
+                  "pbng_tip_components"):
             getattr(lib, f).restype = ctypes.c_int
         lib.pbng_kernel_times.argtypes = [ctypes.c_void_p]
         lib.pbng_kernel_times.restype = ctypes.c_int
@@ -205,6 +208,21 @@ def pbng_tip_decompose_host(off_u, adj_u, off_v, adj_v, P: int, side: int = 0, o
     return out, st.as_dict()
 
 
+def pbng_tip_components(g: DeviceGraph, tip, k: int, side: int = 0, out=None, stream=None):
+    """k-tips of level k from tip numbers `tip` (device int64 tensor of uint64 bits):
+    (int32 tensor of uint32 labels — smallest member id, 0xFFFFFFFF outside the level —, count)."""
+    torch = _torch()
+    n = _n_peel(g, side)
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=g.off_u.device)
+    ncomp = ctypes.c_uint32(0)
+    U, V = g.csrs()
+    _check(load_library().pbng_tip_components(U, V, side, ctypes.c_void_p(tip.data_ptr() if n else None),
+                                              int(k), ctypes.c_void_p(out.data_ptr() if n else None),
+                                              ctypes.byref(ncomp), _stream_ptr(stream)))
+    return out, int(ncomp.value)
+
+
 def pbng_kernel_times() -> dict:
     """Device ms per kernel family of the last call made with OPT_STATS_DEFER."""
     out = (ctypes.c_float * 16)()
@@ -222,3 +240,4 @@ count_butterflies = pbng_count_butterflies
 tip_decompose = pbng_tip_decompose
 tip_plan = pbng_tip_plan
 tip_decompose_host = pbng_tip_decompose_host
+tip_components = pbng_tip_components

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kMidThreads, kMidCtas) k_agg_mid(AggArgs a) {
     const uint32_t u = it.x;
     uint64_t acc = 0;
     auto keep = [u](uint32_t x) { return x != u; };
-    auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
+    auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, u, k, w, acc, upd); };
     mid_agg_one(L, a.offU[u], a.offU[u + 1], a.adjV, it.y, S, &s_nlong, keep, out);
     if (MODE == 0) {
       acc = warp_sum(acc);

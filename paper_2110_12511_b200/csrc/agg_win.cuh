@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     if (t >= n) break;
     const uint32_t u = a.list[t / G].x;
     uint64_t acc = 0;
-    auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, k, w, acc, upd); };
+    auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, u, k, w, acc, upd); };
     const long long ts0 = clock64();
     win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
                 a.win_prof);

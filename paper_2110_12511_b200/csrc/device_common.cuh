@@ -331,4 +331,34 @@ __device__ __forceinline__ void cta_flat_wedges(const L& lists, uint64_t e0, uin
   __syncthreads();
 }
 
+// Union-find over ids for butterfly connectivity (k-tip components, Def. 2
+// P:451-459).  parent[x] <= x always holds: a root is hooked only under a
+// smaller root, so the root of a set is its smallest id and any ancestor read
+// by a racing find is still a valid (smaller) parent.
+__device__ __forceinline__ uint32_t cc_find(uint32_t* parent, uint32_t x) {
+  volatile uint32_t* p = parent;
+  uint32_t y = p[x];
+  while (y != x) {
+    const uint32_t z = p[y];
+    if (z != y) p[x] = z;  // path halving
+    x = y;
+    y = z;
+  }
+  return x;
+}
+
+__device__ __forceinline__ void cc_union(uint32_t* parent, uint32_t a, uint32_t b) {
+  for (;;) {
+    a = cc_find(parent, a);
+    b = cc_find(parent, b);
+    if (a == b) return;
+    if (a < b) {
+      const uint32_t t = a;
+      a = b;
+      b = t;
+    }
+    if (atomicCAS(&parent[a], a, b) == a) return;  // else a was hooked meanwhile: retry
+  }
+}
+
 }  // namespace pbng

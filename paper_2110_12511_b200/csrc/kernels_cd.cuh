@@ -291,6 +291,9 @@ __global__ void __launch_bounds__(512) k_classify_big(const uint2* __restrict__ 
 //                 support[u'] -= C(w(u,u'),2)   (tip batch update, P:987-991:
 //                 updates from different frontier vertices touch disjoint
 //                 butterflies, so they are summed atomically; no floor needed)
+// MODE 2 (LINK):  for every member u of a tip level, every member u' with
+//                 w(u,u') >= 2 (one butterfly {u,u'} at least) joins u's
+//                 union-find set (k-tip components)
 struct AggArgs {
   const uint64_t* __restrict__ offU;
   const uint32_t* __restrict__ adjU;
@@ -313,10 +316,12 @@ struct AggArgs {
   uint32_t win_split;                  // window groups per tier-2 start (>1 for small batches)
   uint32_t win_pre;                    // starts with at most this many lists use precomputed window tables
   bool win_prof;                       // accumulate tier-2 phase clocks (PBNG_TRACE)
+  uint32_t* cc;                        // LINK: union-find parents (k-tip components)
 };
 
 template <int MODE>
-__device__ __forceinline__ void emit(const AggArgs& a, uint32_t k, uint32_t w, uint64_t& acc, unsigned long long& upd) {
+__device__ __forceinline__ void emit(const AggArgs& a, uint32_t u, uint32_t k, uint32_t w, uint64_t& acc,
+                                     unsigned long long& upd) {
   // PEEL skips the liveness test: a peeled partner's support is never read again
   // (selection, snapshots and FD only read live vertices), so decrementing it is
   // harmless and saves a random load per emitted pair
@@ -324,9 +329,11 @@ __device__ __forceinline__ void emit(const AggArgs& a, uint32_t k, uint32_t w, u
     const uint64_t d = choose2(w);
     if (MODE == 0) {
       acc += d;
-    } else {
+    } else if (MODE == 1) {
       red_add_u64(&a.support[k], 0ull - d);
       upd++;
+    } else {
+      cc_union(a.cc, u, k);  // u and k share a butterfly inside the level
     }
   }
 }
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
         const uint32_t wv = vals[s];
         keys[s] = kEmpty;
         vals[s] = 0;
-        emit<MODE>(a, k, wv, acc, upd);
+        emit<MODE>(a, u, k, wv, acc, upd);
       }
     }
     if (MODE == 0) {

@@ -16,6 +16,7 @@
 
 #include "../../include/pbng.h"
 #include "kernels_fd.cuh"
+#include "kernels_level.cuh"
 #include "kernels_relabel.cuh"
 #include "kernels_vp.cuh"
 
@@ -73,6 +74,9 @@ void set_attrs_once() {
     cudaFuncSetAttribute(k_vp_agg_mid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
     cudaFuncSetAttribute(k_agg_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_agg_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+    cudaFuncSetAttribute(k_agg_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
+    cudaFuncSetAttribute(k_agg_mid<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
+    cudaFuncSetAttribute(k_agg_win<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
@@ -426,6 +430,7 @@ struct State {
   unsigned long long* sum_min;    // ∧_cnt = Σ_(u,v) min(d_u, d_v)
   const SideRank* RU;
   const SideRank* RV;
+  uint32_t* cc = nullptr;  // k-tip level retrieval: union-find parents
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -514,6 +519,7 @@ AggArgs agg_args(const State& S, int t) {
   a.win_split = S.win_split;
   a.win_pre = S.win_pre;
   a.win_prof = S.prof;
+  a.cc = S.cc;
   return a;
 }
 
@@ -1064,6 +1070,42 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   if (stats) *stats = st;
 }
 
+// One level of the k-tip hierarchy from the tip numbers: members
+// U_k = {θ >= k}; non-members are deleted from the V lists (the deletion pass
+// of CD), then every member aggregates its wedges inside the
+// level (one-sided tiers, LINK mode) and unions with each member partner it
+// shares a butterfly with.  Returns the number of k-tips.
+uint32_t tip_level(const Dev& g, const uint64_t* tip, uint64_t k, uint32_t* out_comp, cudaStream_t s) {
+  Run r(s);
+  State S;
+  SideRank RU, RV;
+  const Dev gr = relabel(r, g, RU, RV);
+  alloc_state(r, S, gr, true, RU, RV, false);
+  S.cc = r.alloc<uint32_t>(g.nU);
+  uint32_t* minlab = r.alloc<uint32_t>(g.nU);
+  uint32_t* dn = r.alloc<uint32_t>(1);
+  CK(cudaMemsetAsync(dn, 0, 4, r.st));
+  k_level_mark<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, tip, k, S.part, S.cc, minlab);
+  if (g.nV) {
+    CK(cudaMemsetAsync(S.vflag, 1, (size_t)g.nV * 4, r.st));  // every list may hold non-members
+    compact(r, S, 0, true);
+  }
+  reset_tiers(r, S);
+  k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(gr.nU, nullptr, nullptr, gr.offU, gr.adjU, S.ld, S.part, S.support,
+                                               S.tier[0], S.tier[1], S.tier[2], S.tier[3], nullptr, 0, S.c);
+  k_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, gr.offU, gr.adjU, S.ld, S.support, S.tier[0],
+                                                  S.tier[1], S.tier[2], nullptr, 0, S.c);
+  const Counters hc = r.readback(S.c);
+  S.win_split = pick_split(r, hc.ntier[2], gr.nU);
+  launch_agg<2>(r, S, hc.ntier);
+  k_level_minlab<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.part, S.cc, minlab);
+  k_level_label<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.part, S.cc, minlab, out_comp, dn);
+  uint32_t n = 0;
+  CK(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, r.st));
+  CK(cudaStreamSynchronize(r.st));
+  return n;
+}
+
 template <class Fn>
 int guarded(Fn&& fn) {
   g_err.clear();
@@ -1160,6 +1202,18 @@ int pbng_tip_decompose_host(pbng_csr U, pbng_csr V, int side, uint32_t P, uint64
     decompose(g, P, opts, o, stats, s);
     if (nOut) CK(cudaMemcpyAsync(out_tip, dtip, (size_t)nOut * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+  });
+}
+
+int pbng_tip_components(pbng_csr U, pbng_csr V, int side, const uint64_t* tip, uint64_t k, uint32_t* out_comp,
+                        uint32_t* out_ncomp, void* stream) {
+  return guarded([&] {
+    Dev g;
+    orient(U, V, side, g);
+    if (!out_ncomp || (g.nU && (!tip || !out_comp))) fail(PBNG_ERR_ARG, "null pointer");
+    *out_ncomp = 0;
+    if (g.nU == 0) return;
+    *out_ncomp = tip_level(g, tip, k, out_comp, (cudaStream_t)stream);
   });
 }
 

@@ -304,3 +304,58 @@ def test_kernel_times_deferred(pb):
     assert pb.pbng_kernel_times() == {}  # consumed
     _, st2 = pb.pbng_tip_decompose(d, P, opts=pb.OPT_STATS)
     assert set(st2["ms_kernel"]) == set(kt)
+
+
+# ---- k-tip hierarchy retrieval: pbng_tip_components vs oracle.tip_level ----
+
+def _levels(th):
+    u = np.unique(th)
+    top = int(th.max(initial=0))
+    ks = [0, 1, top, top + 1] + [int(x) for x in u[:: max(1, len(u) // 6)]]
+    return sorted(set(ks))
+
+
+def _check_levels(pb, d, gs, th, side, ks):
+    import torch
+    tdev = torch.from_numpy(np.ascontiguousarray(th, np.uint64).view(np.int64)).cuda()
+    for k in ks:
+        lab, n = pb.pbng_tip_components(d, tdev, k, side=side)
+        want, wn = oracle.tip_level(gs, th, k)
+        got = lab.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, want) and n == wn, (gs.name, side, k, n, wn)
+
+
+def test_tip_components_tiny(pb):
+    for g in tiny_corpus(80, 7000):
+        d = dev(pb, g)
+        for side, gs in ((0, g), (1, g.swapped())):
+            th = oracle.bup_tip(gs)
+            _check_levels(pb, d, gs, th, side, _levels(th))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, "2a"])
+def test_tip_components_configs(pb, cfg):
+    g, P = gg.config(cfg)
+    d = dev(pb, g)
+    tip, _ = pb.pbng_tip_decompose(d, P)
+    th = pb.as_u64(tip)
+    assert np.array_equal(th, oracle.bup_tip(g))
+    _check_levels(pb, d, g, th, 0, _levels(th))
+
+
+def test_tip_components_hubs(pb):
+    """Power-law graph with hubs (d_v up to ~5K): starts in all three aggregation tiers."""
+    g = gg.chung_lu(60000, 20000, 300000, 2.1, 2.1, 8000.0, 8000.0, seed=31)
+    d = dev(pb, g)
+    tip, _ = pb.pbng_tip_decompose(d, 32)
+    th = pb.as_u64(tip)
+    assert np.array_equal(th, oracle.bup_tip(g))
+    _check_levels(pb, d, g, th, 0, _levels(th))
+
+
+def test_tip_components_arbitrary_vector(pb):
+    """The level is defined by any vector (members = entries >= k), not only by tip numbers."""
+    g, _ = gg.config(1)
+    rng = np.random.default_rng(5)
+    th = rng.integers(0, 4, g.nU).astype(np.uint64)
+    _check_levels(pb, dev(pb, g), g, th, 0, [0, 1, 2, 3, 4])

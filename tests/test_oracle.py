@@ -169,3 +169,53 @@ def test_certificate_on_config1():
     assert oracle.certify(g, th)
     s_ge = oracle.cert_support_ge(g, th, us=np.arange(0, g.nU, 7))
     assert np.all(s_ge >= th[::7])
+
+
+# ---- k-tip hierarchy retrieval (Def. 2) ----
+
+NOLAB = 0xFFFFFFFF
+
+
+def test_tip_level_golden():
+    graphs = {name: (sizes, edges) for name, sizes, edges, *_ in _parse(os.path.join(GOLD, "survey_graphs.txt"))}
+    for name, k, labels, ncomp in _parse(os.path.join(GOLD, "tip_levels.txt")):
+        nu, nv = map(int, graphs[name][0].split())
+        g = gg.from_edges(nu, nv, _edges(graphs[name][1]))
+        want = [NOLAB if x == "-" else int(x) for x in labels.split()]
+        lab, n = oracle.tip_level(g, oracle.bup_tip(g), int(k))
+        assert list(lab) == want and n == int(ncomp), (name, k)
+        assert brute.k_tips(g, int(k)) == (want, int(ncomp)), (name, k)
+
+
+def test_tip_level_equals_definition2():
+    # the oracle works from tip numbers; brute.k_tips from the 4-tuples alone
+    for g in _tiny_corpus(n=150, seed0=12000):
+        th = oracle.bup_tip(g)
+        for k in range(0, int(th.max(initial=0)) + 2):
+            lab, n = oracle.tip_level(g, th, k)
+            assert (list(lab), n) == brute.k_tips(g, k), (g.name, k)
+
+
+def test_tip_level_blocks_and_nesting():
+    # config 2a: disjoint K_{a,b}; every block is its own k-tip at any k <= its θ
+    shapes = gg.block_sizes(200, 5, 60, seed=2)
+    g, _ = gg.config("2a")
+    th = oracle.bup_tip(g)
+    first = np.cumsum([0] + [a for a, _ in shapes[:-1]])
+    lab, n = oracle.tip_level(g, th, 1)
+    assert n == 200
+    assert np.array_equal(lab, np.repeat(first, [a for a, _ in shapes]).astype(np.uint32))
+    # nesting on config 1: every (k+1)-tip lies inside one k-tip
+    g, _ = gg.config(1)
+    th = oracle.bup_tip(g)
+    ks = np.unique(th)[:: max(1, len(np.unique(th)) // 6)]
+    prev = None
+    for k in ks:
+        lab, n = oracle.tip_level(g, th, int(k))
+        members = th >= k
+        assert np.all((lab != NOLAB) == members)
+        assert np.all(lab[members] <= np.nonzero(members)[0])
+        if prev is not None:
+            for c in np.unique(lab[members]):
+                assert len(np.unique(prev[lab == c])) == 1
+        prev = lab
