@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kMidThreads, kMidCtas) k_agg_mid(AggArgs a) {
     S.vals[i] = 0;
   }
   const uint32_t n = *a.count;
-  const CdLists L{a.adjU, a.offV, a.ld};
+  const auto L = agg_lists<MODE>(a);
   unsigned long long upd = 0;
   for (;;) {
     if (threadIdx.x == 0) {

@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
   uint32_t* bnd = a.win_bnd + (uint64_t)blockIdx.x * a.win_cap;
   const uint32_t G = a.win_split;
   const uint64_t n = (uint64_t)*a.count * G;
-  const CdLists L{a.adjU, a.offV, a.ld};
+  const auto L = agg_lists<MODE>(a);
   unsigned long long upd = 0;
   for (;;) {
     if (threadIdx.x == 0) {
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, u, k, w, acc, upd); };
     const long long ts0 = clock64();
-    win_agg_one(L, a.offU[u], a.offU[u + 1], u, a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, MODE == 2 ? u : a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
                 a.win_prof);
     if (a.win_prof && threadIdx.x == 0) {
       const bool tab = a.offU[u + 1] - a.offU[u] <= a.win_pre;

@@ -139,6 +139,16 @@ struct CdLists {  // CD: live prefix of N_v (dynamic deletion keeps it compact)
     len = ld[v];
   }
 };
+struct PrefixLists {  // k-tip level retrieval: the part of N_v ranked before the start
+  const uint32_t* __restrict__ adjU;
+  const uint64_t* __restrict__ offV;
+  const uint32_t* __restrict__ cut;  // per U-edge (u, v): members of N_v with id < u
+  __device__ __forceinline__ void get(uint64_t e, uint64_t& base, uint32_t& len) const {
+    uint32_t v = adjU[e];
+    base = offV[v];
+    len = cut[e];
+  }
+};
 struct FdLists {  // FD: the segment N_v ∩ U_i of the partition's induced subgraph G_i
   const uint32_t* __restrict__ adjU;
   const uint64_t* __restrict__ offV;

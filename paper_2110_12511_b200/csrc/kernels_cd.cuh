@@ -317,7 +317,20 @@ struct AggArgs {
   uint32_t win_pre;                    // starts with at most this many lists use precomputed window tables
   bool win_prof;                       // accumulate tier-2 phase clocks (PBNG_TRACE)
   uint32_t* cc;                        // LINK: union-find parents (k-tip components)
+  const uint32_t* __restrict__ cut_e;  // LINK: per U-edge (u, v), members of N_v with id < u
 };
+
+// Partner lists of the aggregation tiers: the live prefix of N_v (COUNT, PEEL),
+// or only its members ranked before the start (LINK: a pair is linked once,
+// from its larger id, so each wedge pair is walked once instead of twice)
+template <int MODE>
+__device__ __forceinline__ auto agg_lists(const AggArgs& a) {
+  if constexpr (MODE == 2) {
+    return PrefixLists{a.adjU, a.offV, a.cut_e};
+  } else {
+    return CdLists{a.adjU, a.offV, a.ld};
+  }
+}
 
 template <int MODE>
 __device__ __forceinline__ void emit(const AggArgs& a, uint32_t u, uint32_t k, uint32_t w, uint64_t& acc,
@@ -350,7 +363,7 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
   }
   __syncwarp();
   const uint32_t n = *a.count;
-  const CdLists L{a.adjU, a.offV, a.ld};
+  const auto L = agg_lists<MODE>(a);
   unsigned long long upd = 0;
   const uint32_t wpb = blockDim.x >> 5;
   for (uint32_t i = blockIdx.x * wpb + w; i < n; i += gridDim.x * wpb) {

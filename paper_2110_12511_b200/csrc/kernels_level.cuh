@@ -25,6 +25,36 @@ __global__ void k_level_mark(uint32_t n, const uint32_t* __restrict__ rank, cons
   }
 }
 
+// per U-edge (u, v) of a member u: position of u in the member prefix of N_v
+// (lists are sorted by internal id and stay sorted under deletion), i.e. the
+// number of members of N_v with a smaller id.  Edge-parallel; u by binary
+// search over offU.
+__global__ void k_level_cut(uint32_t nU, uint64_t m, const uint64_t* __restrict__ offU,
+                            const uint32_t* __restrict__ adjU, const uint64_t* __restrict__ offV,
+                            const uint32_t* __restrict__ adjL, const uint32_t* __restrict__ ld,
+                            const uint32_t* __restrict__ part, uint32_t* __restrict__ cut) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = nU;  // largest u with offU[u] <= e
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (offU[mid] <= e) lo = mid; else hi = mid;
+    }
+    const uint32_t u = lo;
+    uint32_t c = 0;
+    if (part[u] == kUnassigned) {
+      const uint32_t v = adjU[e];
+      const uint32_t* p = adjL + offV[v];
+      uint32_t a = 0, b = ld[v];
+      while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (p[mid] < u) a = mid + 1; else b = mid;
+      }
+      c = a;
+    }
+    cut[e] = c;
+  }
+}
+
 // smallest caller id of every set, stored at its root
 __global__ void k_level_minlab(uint32_t n, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ part,
                                uint32_t* cc, uint32_t* minlab) {

@@ -430,7 +430,8 @@ struct State {
   unsigned long long* sum_min;    // ∧_cnt = Σ_(u,v) min(d_u, d_v)
   const SideRank* RU;
   const SideRank* RV;
-  uint32_t* cc = nullptr;  // k-tip level retrieval: union-find parents
+  uint32_t* cc = nullptr;     // k-tip level retrieval: union-find parents
+  uint32_t* cut_e = nullptr;  // ... and per U-edge partner-prefix lengths
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -520,6 +521,7 @@ AggArgs agg_args(const State& S, int t) {
   a.win_pre = S.win_pre;
   a.win_prof = S.prof;
   a.cc = S.cc;
+  a.cut_e = S.cut_e;
   return a;
 }
 
@@ -1074,7 +1076,8 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
 // U_k = {θ >= k}; non-members are deleted from the V lists (the deletion pass
 // of CD), then every member aggregates its wedges inside the
 // level (one-sided tiers, LINK mode) and unions with each member partner it
-// shares a butterfly with.  Returns the number of k-tips.
+// shares a butterfly with; each pair is walked once, from its larger internal
+// id (partner lists cut at the start, k_level_cut).  Returns the number of k-tips.
 uint32_t tip_level(const Dev& g, const uint64_t* tip, uint64_t k, uint32_t* out_comp, cudaStream_t s) {
   Run r(s);
   State S;
@@ -1090,6 +1093,9 @@ uint32_t tip_level(const Dev& g, const uint64_t* tip, uint64_t k, uint32_t* out_
     CK(cudaMemsetAsync(S.vflag, 1, (size_t)g.nV * 4, r.st));  // every list may hold non-members
     compact(r, S, 0, true);
   }
+  S.cut_e = r.alloc<uint32_t>(std::max<uint64_t>(gr.m, 1));
+  if (gr.m)
+    k_level_cut<<<r.nsm * 8, 256, 0, r.st>>>(gr.nU, gr.m, gr.offU, gr.adjU, gr.offV, S.adjL, S.ld, S.part, S.cut_e);
   reset_tiers(r, S);
   k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(gr.nU, nullptr, nullptr, gr.offU, gr.adjU, S.ld, S.part, S.support,
                                                S.tier[0], S.tier[1], S.tier[2], S.tier[3], nullptr, 0, S.c);

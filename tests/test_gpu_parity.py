@@ -359,3 +359,28 @@ def test_tip_components_arbitrary_vector(pb):
     rng = np.random.default_rng(5)
     th = rng.integers(0, 4, g.nU).astype(np.uint64)
     _check_levels(pb, dev(pb, g), g, th, 0, [0, 1, 2, 3, 4])
+
+
+def test_tip_components_config3(pb):
+    """Config 3 at full size: the Def. 2 '>= k butterflies' condition of every level member,
+    counted on the GPU on the level's induced subgraph (verify_hierarchy), and oracle
+    parity of the labels at the top level."""
+    g, P = gg.config(3)
+    d = dev(pb, g)
+    tip, _ = pb.pbng_tip_decompose(d, P)
+    th = pb.as_u64(tip)
+    pos = np.sort(th[th > 0])
+    e = g.edges().astype(np.int64)
+    for q in (0.5, 0.9, 0.999):
+        k = int(pos[int(q * (len(pos) - 1))])
+        lab, n = pb.pbng_tip_components(d, tip, k)
+        lab = lab.cpu().numpy().view(np.uint32)
+        members = th >= k
+        assert np.array_equal(lab != 0xFFFFFFFF, members)
+        assert n == len(np.unique(lab[members]))
+        h = gg.from_edges(g.nU, g.nV, e[members[e[:, 0]]])
+        s = pb.as_u64(pb.pbng_count_butterflies(dev(pb, h)))
+        assert np.all(s[members] >= k), k
+        if q == 0.999:
+            want, wn = oracle.tip_level(g, th, k)
+            assert np.array_equal(lab, want) and n == wn
