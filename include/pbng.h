@@ -170,9 +170,11 @@ int pbng_tip_plan(pbng_csr U, pbng_csr V, int side, uint32_t P, uint32_t opts, u
  *              of u's k-tip, or 0xFFFFFFFF when tip[u] < k.  Labels are
  *              canonical, so results compare bit-exactly.
  *   out_ncomp  HOST pointer: number of k-tips (components) in the level.
- * Computed by the one-sided aggregation tiers (LINK mode: union-find over
- * pairs with w >= 2) on the level's subgraph.  Errors as above; PBNG_ERR_ARG
- * for null pointers. */
+ * Computed on the level's subgraph (non-members deleted from the V lists) by
+ * the one-sided aggregation tiers in LINK mode: each member u aggregates
+ * w(u, u') over partners u' ranked before it and unions with every u' with
+ * w >= 2 (lock-free union-find).  Errors as above; PBNG_ERR_ARG for null
+ * pointers.  Synchronous like the other entry points. */
 int pbng_tip_components(pbng_csr U, pbng_csr V, int side, const uint64_t* tip, uint64_t k, uint32_t* out_comp,
                         uint32_t* out_ncomp, void* stream);
 
