@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, u, k, w, acc, upd); };
     const long long ts0 = clock64();
-    win_agg_one(L, a.offU[u], a.offU[u + 1], u, MODE == 2 ? u : a.nU, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, MODE == 2 ? u : a.idspace, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
                 a.win_prof);
     if (a.win_prof && threadIdx.x == 0) {
       const bool tab = a.offU[u + 1] - a.offU[u] <= a.win_pre;

@@ -57,6 +57,7 @@ struct Counters {
   uint32_t pad0;
   unsigned long long live_wc;    // range pass: Σ wc over live
   unsigned long long live_n;     // range pass: live count
+  unsigned long long max_live;   // range pass: 1 + largest live id
   // cumulative
   unsigned long long updates;    // C(w,2) decrements
   unsigned long long ld2_drop;   // compaction: decrease of Σ_v ld_v^2
@@ -318,6 +319,7 @@ struct AggArgs {
   bool win_prof;                       // accumulate tier-2 phase clocks (PBNG_TRACE)
   uint32_t* cc;                        // LINK: union-find parents (k-tip components)
   const uint32_t* __restrict__ cut_e;  // LINK: per U-edge (u, v), members of N_v with id < u
+  uint32_t idspace;                    // tier-2 windows cover partner ids [0, idspace) (COUNT, PEEL)
 };
 
 // Partner lists of the aggregation tiers: the live prefix of N_v (COUNT, PEEL),
@@ -418,9 +420,10 @@ __global__ void __launch_bounds__(1024) k_range_hist(uint32_t nU, const uint32_t
     hn[b] = 0;
   }
   __syncthreads();
-  unsigned long long tw = 0, tn = 0;
+  unsigned long long tw = 0, tn = 0, mx = 0;
   for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nU; u += (uint64_t)gridDim.x * blockDim.x) {
     if (part[u] != kUnassigned) continue;
+    mx = u + 1;
     const uint64_t s = support[u];
     init[u] = s;
     const uint32_t k = support_key(s);
@@ -439,9 +442,12 @@ __global__ void __launch_bounds__(1024) k_range_hist(uint32_t nU, const uint32_t
   }
   tw = warp_sum(tw);
   tn = warp_sum(tn);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
   if (lane_id() == 0 && tn) {
     atomicAdd(&c->live_wc, tw);
     atomicAdd(&c->live_n, tn);
+    atomicMax(&c->max_live, mx);
   }
 }
 

@@ -432,6 +432,7 @@ struct State {
   const SideRank* RV;
   uint32_t* cc = nullptr;     // k-tip level retrieval: union-find parents
   uint32_t* cut_e = nullptr;  // ... and per U-edge partner-prefix lengths
+  uint32_t idspace = 0;       // 1 + largest live id (tier-2 window range; ids above are all peeled)
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -446,6 +447,7 @@ uint32_t choose_slots(const Run& r, uint32_t nU) {
 
 void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank& RU, const SideRank& RV, bool vp) {
   S.g = g;
+  S.idspace = g.nU;
   S.vp = vp;
   S.RU = &RU;
   S.RV = &RV;
@@ -522,6 +524,7 @@ AggArgs agg_args(const State& S, int t) {
   a.win_prof = S.prof;
   a.cc = S.cc;
   a.cut_e = S.cut_e;
+  a.idspace = S.idspace;
   return a;
 }
 
@@ -622,7 +625,7 @@ void count_live(Run& r, State& S) {
                                                   S.tier[1], S.tier[2], nullptr, 0, S.c);
   r.post(PBNG_K_CLASSIFY);
   const Counters hc = r.readback(S.c);
-  S.win_split = pick_split(r, hc.ntier[2], S.g.nU);
+  S.win_split = pick_split(r, hc.ntier[2], S.idspace);
   launch_agg<0>(r, S, hc.ntier);
 }
 
@@ -688,7 +691,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
     // --- partition start: ⋈^init snapshot + weighted support histogram
     CK(cudaMemsetAsync(S.hist_w, 0, kBins * 8, r.st));
     CK(cudaMemsetAsync(S.hist_n, 0, kBins * 4, r.st));
-    CK(cudaMemsetAsync(&S.c->live_wc, 0, 16, r.st));
+    CK(cudaMemsetAsync(&S.c->live_wc, 0, 24, r.st));
     r.pre(PBNG_K_RANGE);
     k_range_hist<<<r.nsm, 1024, hist_smem(), r.st>>>(nU, S.part, S.support, S.wc, S.init, S.hist_w, S.hist_n,
                                                      S.c);
@@ -697,6 +700,12 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
     CK(cudaMemcpyAsync(hn.data(), S.hist_n, kBins * 4, cudaMemcpyDeviceToHost, r.st));
     const Counters hc0 = r.readback(S.c);
     if (hc0.live_n == 0) break;
+#ifndef PBNG_LIVE_IDSPACE
+#define PBNG_LIVE_IDSPACE 1
+#endif
+    // the live set only shrinks inside a partition: partners above the
+    // largest live id are all peeled, so tier-2 windows stop there
+    if (PBNG_LIVE_IDSPACE) S.idspace = (uint32_t)hc0.max_live;
     // --- find_range: smallest bin whose cumulative work reaches tgt
     uint64_t bound = kInf;
     if (pid + 1 < P) {
@@ -762,7 +771,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         count_live(r, S);
         st.recounts++;
       } else {
-        S.win_split = pick_split(r, hc.ntier[2], nU);
+        S.win_split = pick_split(r, hc.ntier[2], S.idspace);
         launch_agg<1>(r, S, hc.ntier);
         if (del) compact(r, S, epoch);
       }
