@@ -69,6 +69,12 @@ def _load():
         _lib.oracle_cert_support_ge.restype = ctypes.c_int
         _lib.oracle_cert_levels.argtypes = base + [ctypes.c_void_p] * 4 + [ctypes.c_uint64, ctypes.c_void_p]
         _lib.oracle_cert_levels.restype = ctypes.c_int64
+        _lib.oracle_cert_sort_lists.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 4
+        _lib.oracle_cert_sort_lists.restype = ctypes.c_int
+        _lib.oracle_cert_pass.argtypes = base + [ctypes.c_void_p] * 4
+        _lib.oracle_cert_pass.restype = ctypes.c_int
+        _lib.oracle_cert_levels_induced.argtypes = base + [ctypes.c_void_p] * 5 + [ctypes.c_uint64, ctypes.c_void_p]
+        _lib.oracle_cert_levels_induced.restype = ctypes.c_int64
     return _lib
 
 
@@ -164,6 +170,50 @@ def cert_levels(g, theta, levels=None):
         raise MemoryError("oracle_cert_levels failed")
     del keep
     return int(bad), (int(lev[first.value]) if bad else None)
+
+
+def _levels(th):
+    """Distinct θ' values with their members (ascending id within a level)."""
+    order = np.argsort(th, kind="stable").astype(np.uint32)
+    vals = th[order]
+    uniq, starts = np.unique(vals, return_index=True)
+    off = np.append(starts, len(vals)).astype(np.uint64)
+    return np.ascontiguousarray(uniq, np.uint64), off, np.ascontiguousarray(order, np.uint32)
+
+
+def cert_one_pass(g, theta, progress=None):
+    """One-pass certificate (certificate.c, oracle_cert_pass + oracle_cert_levels_induced):
+    returns (support, s_ge, number of failing (C) levels, first failing level or None).
+    `support` equals count(g) and `s_ge` equals cert_support_ge(g, θ') (each unordered
+    pair walked once from its smaller (θ', id) end); `progress` = optional uint64
+    numpy array of one element, incremented per finished vertex (for long runs)."""
+    keep, ptrs = _csr(g)
+    lib = _load()
+    th = np.ascontiguousarray(theta, np.uint64)
+    adj_s = np.empty(g.m, np.uint32)
+    lib.oracle_cert_sort_lists(g.nV, ptrs[2], ptrs[3], th.ctypes.data, adj_s.ctypes.data)
+    sup = np.zeros(g.nU, np.uint64)
+    sge = np.zeros(g.nU, np.uint64)
+    ptrs_s = [ptrs[0], ptrs[1], ptrs[2], adj_s.ctypes.data]
+    if lib.oracle_cert_pass(g.nU, g.nV, *ptrs_s, th.ctypes.data, sup.ctypes.data, sge.ctypes.data,
+                            None if progress is None else progress.ctypes.data):
+        raise MemoryError("oracle_cert_pass failed")
+    lev, off, mem = _levels(th)
+    first = ctypes.c_uint64(0)
+    bad = lib.oracle_cert_levels_induced(g.nU, g.nV, *ptrs_s, th.ctypes.data, sge.ctypes.data, lev.ctypes.data,
+                                         off.ctypes.data, mem.ctypes.data if len(mem) else None, len(lev),
+                                         ctypes.byref(first))
+    if bad < 0:
+        raise MemoryError("oracle_cert_levels_induced failed")
+    del keep
+    return sup, sge, int(bad), (int(lev[first.value]) if bad else None)
+
+
+def certify_one_pass(g, theta) -> bool:
+    """certify() by the one-pass certificate: (A) s_ge >= θ' and (C) on every level."""
+    th = np.ascontiguousarray(theta, np.uint64)
+    _, sge, bad, _ = cert_one_pass(g, th)
+    return bool(np.all(sge >= th)) and bad == 0
 
 
 def certify(g, theta) -> bool:

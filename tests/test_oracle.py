@@ -219,3 +219,53 @@ def test_tip_level_blocks_and_nesting():
             for c in np.unique(lab[members]):
                 assert len(np.unique(prev[lab == c])) == 1
         prev = lab
+
+
+def test_one_pass_certificate_equals_per_vertex_certificate():
+    """certificate.c one-pass functions (each unordered pair once, induced level runs):
+    counts equal oracle_count, s_ge equals oracle_cert_support_ge, verdicts equal certify()
+    on the Definition-2 θ, every ±1 mutation and random vectors."""
+    rng = np.random.default_rng(21)
+    for g in _tiny_corpus(n=120, seed0=15000):
+        want = np.array(brute.tip_by_definition(g), np.uint64)
+        sup, sge, bad, _ = oracle.cert_one_pass(g, want)
+        assert np.array_equal(sup, oracle.count(g))
+        assert np.array_equal(sup, np.array(brute.butterflies(g)[0], np.uint64))
+        assert np.array_equal(sge, oracle.cert_support_ge(g, want))
+        assert bad == 0 and oracle.certify_one_pass(g, want)
+        for u in range(g.nU):
+            for d in (-1, 1):
+                if int(want[u]) + d < 0:
+                    continue
+                cand = want.copy()
+                cand[u] = np.uint64(int(cand[u]) + d)
+                assert not oracle.certify_one_pass(g, cand), (g.name, u, d)
+        for _ in range(5):
+            cand = rng.integers(0, sup + 2).astype(np.uint64)
+            assert oracle.certify_one_pass(g, cand) == bool(np.array_equal(cand, want))
+
+
+def test_one_pass_certificate_on_config1():
+    g, _ = gg.config(1)
+    th = oracle.bup_tip(g)
+    sup, sge, bad, _ = oracle.cert_one_pass(g, th)
+    assert np.array_equal(sup, oracle.count(g)) and bad == 0 and np.all(sge >= th)
+
+
+def test_brute_init_support_pins():
+    """brute.init_support (the ⋈^init checker) against what fixes it without itself:
+    one partition -> the 4-tuple counts; K_{a,b} with any partition vector -> closed form
+    (#u' != u with part[u'] >= part[u]) * C(b,2); partitions ordered like θ -> s_ge of the
+    certificate's (A) (u' with θ' >= θ'_u)."""
+    rng = np.random.default_rng(31)
+    for g in _tiny_corpus(n=60, seed0=16000):
+        cu = brute.butterflies(g)[0]
+        assert brute.init_support(g, [0] * g.nU) == cu
+        th = oracle.bup_tip(g)
+        assert brute.init_support(g, [int(x) for x in th]) == list(oracle.cert_support_ge(g, th))
+    for a, b in ((2, 2), (3, 4), (5, 3), (4, 6)):
+        g = gg.complete(a, b)
+        for _ in range(5):
+            part = [int(x) for x in rng.integers(0, 3, a)]
+            want = [sum(1 for x in range(a) if x != u and part[x] >= part[u]) * comb(b, 2) for u in range(a)]
+            assert brute.init_support(g, part) == want
