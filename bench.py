@@ -6,8 +6,16 @@ One "step" = one full tip decomposition (count + CD + FD, every §8(a) row) of t
 workload graph through the C ABI (pbng_tip_decompose) with the CSR already in HBM.
 N > 1 (torchrun): every rank decomposes its own replica (the path does not shard —
 DESIGN.md "replicas only"); value = wedges of all ranks / max-over-ranks time.
-`--impl reference` times the CPU oracle (oracle/, single thread) on a bounded
-sample of the same workload instead.  Prints ONE JSON line on rank 0.
+`--impl reference` times the CPU oracle (oracle/, single thread: plain count +
+sequential bottom-up peeling) decomposing a bounded sample of the same workload
+(the subgraph induced by a seeded 1% sample of the peel side with all of V)
+instead.  Prints ONE JSON line on rank 0.
+
+Timing: K steps with no instrumentation (opts = 0; the library's work counters
+are always filled).  Then one separate stats step (PBNG_OPT_STATS_DEFER: a CUDA
+event pair around every launch, on the launch stream) gives the device time per
+kernel family for the roofline; its own duration is reported beside the timed
+steps so the cost of the events is visible.
 """
 from __future__ import annotations
 
@@ -122,6 +130,42 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- oracle arm
+def host_cpu():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def induced_sample(g, frac, seed=2110):
+    """Subgraph induced by a seeded random `frac` of the peel-side vertices and all of V
+    (the same degree structure, thinned): a bounded decomposition for the CPU oracle."""
+    import graphgen as gg
+    rng = np.random.default_rng(seed)
+    keep = rng.random(g.nU) < frac
+    new_id = np.cumsum(keep) - 1
+    du = np.diff(g.off_u.astype(np.int64))
+    u_of_e = np.repeat(np.arange(g.nU, dtype=np.int64), du)
+    sel = keep[u_of_e]
+    edges = np.stack([new_id[u_of_e[sel]], g.adj_u[sel].astype(np.int64)], axis=1)
+    return gg.from_edges(int(keep.sum()), g.nV, edges)
+
+
+def time_oracle_bup(sub):
+    """Seconds and wedges of the oracle's full decomposition (count + bottom-up peeling) of `sub`."""
+    import oracle
+    st = oracle.Stats()
+    t = time.perf_counter()
+    oracle.bup_tip(sub, st)
+    dt = time.perf_counter() - t
+    return dt, st.wedges
+
+
 def oracle_sample(g, target_wedges, seed=12345):
     """Seeded random sample of peel-side vertices whose traversal totals ~target_wedges."""
     du = np.diff(g.off_u.astype(np.int64))
@@ -145,6 +189,12 @@ def time_oracle(g, target_wedges):
     return st.wedges / dt, dt, len(us), st.wedges
 
 
+def sample_desc(g, sub, frac, wedges, secs):
+    return (f"oracle_bup_tip (plain one-sided count + sequential bottom-up peeling, oracle/oracle.c) decomposing "
+            f"the subgraph induced by a seeded {frac:.0%} sample of the workload's peel side with all of V "
+            f"(nU={sub.nU} of {g.nU}, m={sub.m}); {wedges} oracle wedges in {secs:.1f} s; single thread")
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -152,25 +202,22 @@ def run_reference(args):
     import oracle
     oracle.build_lib()
     g, P, _ = load_graph(args.config)
-    target = args.ref_wedges
-    for _ in range(args.warmup):
-        time_oracle(g, target)
-    rates, secs, wsum = [], 0.0, 0
-    n = 0
+    sub = induced_sample(g, args.ref_frac)
+    for _ in range(min(args.warmup, 1)):  # the oracle has no warm-up effects beyond page-in
+        time_oracle_bup(sub)
+    secs, wsum = 0.0, 0
     for _ in range(args.steps):
-        r, dt, n, w = time_oracle(g, target)
-        rates.append(r)
+        dt, w = time_oracle_bup(sub)
         secs += dt
         wsum += w
     value = wsum / secs
-    sample = (f"oracle_count_subset (one-sided wedge traversal + C(w,2) aggregation, the oracle's traversal "
-              f"kernel) over {n} seeded random peel-side vertices of the workload, {wsum // args.steps} wedges "
-              f"per step; single thread")
+    sample = sample_desc(g, sub, args.ref_frac, wsum // args.steps, secs / args.steps)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "uint64",
             "data": "synthetic", "config": workload_desc(args.config, g, P),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -198,7 +245,7 @@ def roofline(stats_list, peaks):
     for st in stats_list:
         for k, v in st["ms_kernel"].items():
             ms[k] = ms.get(k, 0.0) + v
-    agg_ms = sum(ms.get(k, 0.0) for k in ("agg_warp", "agg_cta", "agg_heavy"))
+    agg_ms = sum(ms.get(k, 0.0) for k in ("agg_warp", "agg_cta", "agg_hash"))
     dominant = max(ms, key=ms.get) if ms else None
     W = sum(s["wedges_count"] + s["wedges_cd"] for s in stats_list)
     S = sum(s["uv_steps"] - s["uv_steps_fd"] for s in stats_list)
@@ -218,7 +265,8 @@ def roofline(stats_list, peaks):
                             if k in t}
         except Exception:
             traffic = None
-    return {"kernel": "wedge aggregation family: k_agg_warp / k_agg_mid / k_agg_win and the vertex-priority k_vp_agg_* (count + CD peel)", "bound": "hbm",
+    return {"kernel": "wedge aggregation family: k_agg_warp / k_agg_hash / k_agg_win and the vertex-priority "
+                      "k_vp_agg_* (count + CD peel), device time from the stats step", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_launch": traffic_note, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
             else "fallback 6650 GB/s (B200_PROFILING.md)",
@@ -245,9 +293,7 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
     out = torch.empty(g.nU, dtype=torch.int64, device=f"cuda:{local}")
-    # per-launch event pairs are recorded inside the timed region; their elapsed
-    # times are summed after it (pbng_kernel_times), so the queries cost nothing here
-    opts = pb.OPT_STATS_DEFER
+    opts = 0  # timed steps carry no instrumentation
     for i in range(args.warmup):
         pb.pbng_tip_decompose(d, P, opts=opts, out=out)
     torch.cuda.synchronize()
@@ -265,10 +311,18 @@ def run_gpu(args):
         e1.record(stream)
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
-        st["ms_kernel"] = pb.pbng_kernel_times()
         stats.append(st)
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    # ---- stats step (outside the timed region): device time per kernel family
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _, st_stats = pb.pbng_tip_decompose(d, P, opts=pb.OPT_STATS_DEFER, out=out)
+    e1.record(stream)
+    e1.synchronize()
+    stats_step_ms = e0.elapsed_time(e1)
+    st_stats["ms_kernel"] = pb.pbng_kernel_times()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -313,10 +367,12 @@ def run_gpu(args):
         peaks = json.load(open(pp))
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rate, dt, n, w = time_oracle(g, args.ref_wedges * 4)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle_count_subset over {n} seeded random peel-side vertices of the workload "
-                         f"({w} wedges, {dt:.1f} s, single thread)"}
+        import oracle
+        oracle.build_lib()
+        sub = induced_sample(g, args.ref_frac)
+        dt, w = time_oracle_bup(sub)
+        cpu = {"value": w / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": sample_desc(g, sub, args.ref_frac, w, dt), **host_cpu()}
     st = stats[-1]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -326,11 +382,13 @@ def run_gpu(args):
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "seconds_per_decomposition": max_ms / args.steps / 1000,
         "e2e": e2e, "gpu_launches": int(sum(s["launches"] for s in stats)),
-        "roofline": roofline(stats, peaks), "cpu_baseline": cpu, "clocks": clocks,
+        "roofline": {**roofline([st_stats], peaks), "stats_step_ms": stats_step_ms}, "cpu_baseline": cpu,
+        "clocks": clocks,
         "detail": {"wedges_per_step": wedges_step, "wedges_count": st["wedges_count"], "wedges_cd": st["wedges_cd"],
                    "wedges_fd": st["wedges_fd"], "rho_cd_iters": st["rho_cd_iters"],
                    "partitions_used": st["partitions_used"], "recounts": st["recounts"],
                    "fd_rounds_max": st["fd_rounds_max"], "support_updates": st["support_updates"],
+                   "impl_win": st["impl"], "impl_hash": st["impl_hash"],
                    "ms_phase": {"count": st["ms_count"], "cd": st["ms_cd"], "fd_build": st["ms_fd_build"],
                                 "fd": st["ms_fd"]}, "gen_seconds": gen_s},
     }
@@ -382,7 +440,9 @@ def main():
     ap.add_argument("--impl", default="pbng", choices=["pbng", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-wedges", type=float, default=5e8, help="oracle wedges per reference step")
+    ap.add_argument("--ref-wedges", type=float, default=5e8, help="(unused; kept for old scripts)")
+    ap.add_argument("--ref-frac", type=float, default=0.01,
+                    help="peel-side fraction of the induced sample the oracle decomposes")
     ap.add_argument("--ablation", action="store_true", help="PBNG / PBNG- / PBNG-- / one-sided count, both sides")
     args = ap.parse_args()
     if args.ablation:

@@ -23,8 +23,11 @@
  *              (tip decomposition peels one vertex set).
  *   Memory     pbng_* (except *_host) take DEVICE pointers for the graph and
  *              the outputs, caller-allocated and caller-owned.  The library
- *              allocates its own scratch stream-ordered on `stream` and frees
- *              it before returning; it keeps no global state between calls.
+ *              allocates its scratch stream-ordered on `stream` from a private
+ *              memory pool per device and frees it before returning; freed
+ *              scratch stays mapped in that pool for the next call until
+ *              pbng_release_memory() is called.  The device's default memory
+ *              pool is not touched.  No other state is kept between calls.
  *   stream     a cudaStream_t passed as void* (NULL = legacy default stream).
  *   Sync       every call returns only after its work on `stream` completed
  *              (the CD loop reads counters back to the host), so outputs are
@@ -75,18 +78,20 @@ typedef struct {
   uint32_t launches;         /* kernels launched by this call */
   uint32_t pad;
   uint64_t impl[4];          /* implementation counters (tier-2 bitmap windows, repeat-table overflows,
-                                dense passes, -) */
+                                dense passes, CD starts aggregated in grid mode) */
   /* device time per kernel family, filled only with PBNG_OPT_STATS (CUDA events
    * recorded on `stream` around each launch): index by PBNG_K_* */
   float ms_kernel[16];
+  uint64_t impl_hash[4];     /* tier-1 hash aggregation (count + CD): starts, starts split into id-window
+                                groups, groups of those starts, starts passed on to the bitmap tier */
 } pbng_stats;
 
 enum {
   PBNG_K_INIT = 0,      /* k_init_u / k_init_v / validation */
   PBNG_K_CLASSIFY = 1,  /* k_classify: per-vertex wedge work and tier routing */
   PBNG_K_AGG_WARP = 2,  /* k_agg_warp: tier-0 wedge aggregation (warp per vertex) */
-  PBNG_K_AGG_CTA = 3,   /* k_agg_mid / k_agg_win (+ vertex-priority variants): CTA-per-start aggregation */
-  PBNG_K_AGG_HEAVY = 4, /* (unused) */
+  PBNG_K_AGG_CTA = 3,   /* k_agg_win, k_vp_agg_mid / k_vp_agg_win: CTA-per-start windowed-bitmap tier */
+  PBNG_K_AGG_HASH = 4,  /* k_agg_hash / k_vp_agg_hash: CTA-per-start packed-hash tier */
   PBNG_K_SELECT = 5,    /* k_select: frontier selection + compaction */
   PBNG_K_RANGE = 6,     /* k_range_hist: ⋈^init snapshot + range histogram */
   PBNG_K_COMPACT = 7,   /* k_compact*: dynamic deletion */
@@ -185,6 +190,11 @@ int pbng_tip_components(pbng_csr U, pbng_csr V, int side, const uint64_t* tip, u
  * out_ms: host array of PBNG_K_NUM floats.  Returns PBNG_ERR_ARG if out_ms is
  * NULL; all zeros if no deferred call was made since the last query. */
 int pbng_kernel_times(float* out_ms);
+
+/* Return the scratch memory the library's private pools keep mapped (on every
+ * device used so far) to the driver.  Safe to call at any time when no pbng_*
+ * call is running; the next call maps its scratch again. */
+int pbng_release_memory(void);
 
 /* Message for the last non-OK return on this thread ("" if none). */
 const char* pbng_last_error(void);

@@ -30,10 +30,10 @@ OK, ERR_ARG, ERR_GRAPH, ERR_OOM, ERR_CUDA = 0, 1, 2, 3, 4
 OPT_NO_RECOUNT, OPT_NO_DELETE, OPT_VALIDATE, OPT_STATS, OPT_FORCE_RECOUNT, OPT_ONESIDED_COUNT = 1, 2, 4, 8, 16, 32
 OPT_FD_GRID, OPT_STATS_DEFER = 64, 128
 MAX_P = 4096
-KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_heavy", "select", "range", "compact",
+KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_hash", "select", "range", "compact",
                    "fd_build", "fd", "count_vp")
 EXPORTS = ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
-           "pbng_tip_components", "pbng_kernel_times", "pbng_last_error", "pbng_version")
+           "pbng_tip_components", "pbng_kernel_times", "pbng_release_memory", "pbng_last_error", "pbng_version")
 
 
 class PbngError(RuntimeError):
@@ -56,11 +56,12 @@ class Stats(ctypes.Structure):
                 ("ms_fd_build", ctypes.c_float), ("ms_fd", ctypes.c_float),
                 ("uv_steps", ctypes.c_uint64), ("uv_steps_fd", ctypes.c_uint64), ("updates_fd", ctypes.c_uint64),
                 ("launches", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("impl", ctypes.c_uint64 * 4),
-                ("ms_kernel", ctypes.c_float * 16)]
+                ("ms_kernel", ctypes.c_float * 16), ("impl_hash", ctypes.c_uint64 * 4)]
 
     def as_dict(self) -> dict:
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("pad", "ms_kernel", "impl")}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("pad", "ms_kernel", "impl", "impl_hash")}
         d["impl"] = list(self.impl)
+        d["impl_hash"] = list(self.impl_hash)
         d["ms_kernel"] = {name: round(float(self.ms_kernel[i]), 4) for i, name in enumerate(KERNEL_FAMILIES)
                           if self.ms_kernel[i]}
         return d
@@ -89,6 +90,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             getattr(lib, f).restype = ctypes.c_int
         lib.pbng_kernel_times.argtypes = [ctypes.c_void_p]
         lib.pbng_kernel_times.restype = ctypes.c_int
+        lib.pbng_release_memory.argtypes = []
+        lib.pbng_release_memory.restype = ctypes.c_int
         lib.pbng_last_error.restype = ctypes.c_char_p
         lib.pbng_last_error.argtypes = []
         lib.pbng_version.restype = ctypes.c_char_p
@@ -228,6 +231,11 @@ def pbng_kernel_times() -> dict:
     out = (ctypes.c_float * 16)()
     _check(load_library().pbng_kernel_times(ctypes.cast(out, ctypes.c_void_p)))
     return {name: round(float(out[i]), 4) for i, name in enumerate(KERNEL_FAMILIES) if out[i]}
+
+
+def pbng_release_memory() -> None:
+    """Return the library's cached scratch (private per-device pools) to the driver."""
+    _check(load_library().pbng_release_memory())
 
 
 def as_u64(t) -> np.ndarray:

@@ -383,7 +383,9 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
                                             uint32_t idspace, uint32_t g, uint32_t G,
                                             const uint32_t* __restrict__ partner, WinSmem& S, WinShared& sh,
                                             uint32_t* __restrict__ bnd, uint32_t pre_lists, Emit& emit,
-                                            unsigned long long* dbg, bool prof, const Pass2& pass2 = Pass2()) {
+                                            Counters* cnt, bool prof, const Pass2& pass2 = Pass2()) {
+  unsigned long long* dbg = cnt->dbg;        // path counters
+  unsigned long long* prof_clk = cnt->prof;  // PBNG_TRACE phase clocks: [1] tables, [2] bitmap, [3] dense
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
   const uint64_t nl = e1 - e0;
   const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
@@ -474,7 +476,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     }
   }
   __syncthreads();
-  if (prof && tid == 0) atomicAdd(&dbg[5], (unsigned long long)(clock64() - tp0));
+  if (prof && tid == 0) atomicAdd(&prof_clk[1], (unsigned long long)(clock64() - tp0));
   for (uint32_t k = k0; k < k1; k++) {
     const uint64_t wa = (uint64_t)k * kWinIds;
     const uint64_t wb = wa + kWinIds < idspace ? wa + kWinIds : idspace;
@@ -520,7 +522,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<1>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       __syncthreads();
       const long long tm1 = clock64();
-      if (prof && tid == 0) atomicAdd(&dbg[6], (unsigned long long)(tm1 - tm0));
+      if (prof && tid == 0) atomicAdd(&prof_clk[2], (unsigned long long)(tm1 - tm0));
       const bool over = sh.over != 0;
       const uint32_t nd = min(sh.ndup, kWinDupCap);
       if (Pass2::kOn && !over && nd) {
@@ -672,7 +674,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     // the repeat table's memory held touched words: empty it again
     for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;
     __syncthreads();
-    if (prof && tid == 0) atomicAdd(&dbg[7], (unsigned long long)(clock64() - td0));
+    if (prof && tid == 0) atomicAdd(&prof_clk[3], (unsigned long long)(clock64() - td0));
   }
 }
 
@@ -700,7 +702,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     uint64_t acc = 0;
     auto out = [&](uint32_t k, uint32_t w) { emit<MODE>(a, u, k, w, acc, upd); };
     const long long ts0 = clock64();
-    win_agg_one(L, a.offU[u], a.offU[u + 1], u, MODE == 2 ? u : a.idspace, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c->dbg,
+    win_agg_one(L, a.offU[u], a.offU[u + 1], u, MODE == 2 ? u : a.idspace, t % G, G, a.adjV, S, sh, bnd, a.win_pre, out, a.c,
                 a.win_prof);
     if (a.win_prof && threadIdx.x == 0) {
       const bool tab = a.offU[u + 1] - a.offU[u] <= a.win_pre;
@@ -719,4 +721,53 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     upd = warp_sum(upd);
     if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
   }
+}
+
+// ---------------------------------------------------------------- grid mode
+constexpr uint32_t kGridStarts = 64;  // batches with at most this many tier-2 starts use grid mode
+
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+// CD peel of a batch with only a few tier-2 starts (the last partitions peel
+// the highest-degree vertices a handful at a time): one CTA per start (or per
+// window group) would leave most SMs idle while it walks up to ~10^5 lists.
+// Instead every SM walks a share of the starts' lists and counts w(s, x) in a
+// dense per-start array in global memory (L2-resident: the live id range is
+// small by then), then a sweep emits C(w,2) and zeroes the array again.  This
+// is the paper's private n-element wedge array, shared by the
+// whole GPU for one start.
+__global__ void __launch_bounds__(256) k_grid_mark(const uint2* __restrict__ list, uint32_t n2, CdLists L,
+                                                   const uint64_t* __restrict__ offU,
+                                                   const uint32_t* __restrict__ adjV, uint32_t idspace,
+                                                   uint32_t* __restrict__ cnt) {
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = 0; i < n2; i++) {
+    const uint32_t u = list[i].x;
+    uint32_t* c = cnt + (uint64_t)i * idspace;
+    auto f = [&](bool ok, uint32_t x, uint64_t) {
+      if (ok && x != u && x < idspace) atomicAdd(&c[x], 1u);
+    };
+    const uint64_t e0 = offU[u], e1 = offU[u + 1];
+    for (uint64_t ch = e0 + gw * 32; ch < e1; ch += nw * 32)
+      warp_chunk(L, ch, ch + 32 < e1 ? ch + 32 : e1, adjV, 0xFFFFFFFFu, nullptr, nullptr, 0, f);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_grid_sweep(uint32_t n2, uint32_t idspace, uint32_t* __restrict__ cnt,
+                                                    uint64_t* support, Counters* c) {
+  unsigned long long upd = 0;
+  const uint64_t n = (uint64_t)n2 * idspace;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = cnt[j];
+    if (w) {
+      cnt[j] = 0u;
+      if (w >= 2) {
+        red_add_u64(&support[j % idspace], 0ull - choose2(w));
+        upd++;
+      }
+    }
+  }
+  upd = warp_sum(upd);
+  if (lane_id() == 0 && upd) atomicAdd(&c->updates, upd);
 }

@@ -138,6 +138,7 @@ struct CdLists {  // CD: live prefix of N_v (dynamic deletion keeps it compact)
     base = offV[v];
     len = ld[v];
   }
+  __device__ __forceinline__ uint32_t mid(uint64_t e) const { return adjU[e]; }
 };
 struct PrefixLists {  // k-tip level retrieval: the part of N_v ranked before the start
   const uint32_t* __restrict__ adjU;
@@ -148,6 +149,7 @@ struct PrefixLists {  // k-tip level retrieval: the part of N_v ranked before th
     base = offV[v];
     len = cut[e];
   }
+  __device__ __forceinline__ uint32_t mid(uint64_t e) const { return adjU[e]; }
 };
 struct FdLists {  // FD: the segment N_v ∩ U_i of the partition's induced subgraph G_i
   const uint32_t* __restrict__ adjU;

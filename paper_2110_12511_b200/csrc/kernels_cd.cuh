@@ -28,6 +28,7 @@ constexpr uint32_t kClassBig = 2048;            // classify: degree handled by a
 constexpr uint32_t kBins = 14336;
 __host__ __device__ __forceinline__ uint32_t support_key(uint64_t s) {
   if (s < 256) return (uint32_t)s;
+  if (s >> 63) return kBins - 1;  // (unreachable for real counts) keep the key inside the histogram
 #ifdef __CUDA_ARCH__
   uint32_t e = 63 - __clzll((long long)s);
 #else
@@ -67,6 +68,7 @@ struct Counters {
   unsigned long long dbg[4];          // tier-2 internals: bitmap windows, overflows, dense passes, -
   unsigned long long prof[4];         // tier-2 clock64 of CTA thread 0: starts with tables, precompute, bitmap windows, dense passes
   unsigned long long prof2[4];        // tier-2: cycles / count of starts without tables, count of starts with tables, -
+  unsigned long long hashc[4];        // tier 1: starts, starts split into groups, groups, starts passed on to tier 2
 };
 
 // ---------------------------------------------------------------- init
@@ -127,7 +129,8 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
                            const uint64_t* __restrict__ offU, const uint32_t* __restrict__ adjU,
                            const uint32_t* __restrict__ ld, const uint32_t* __restrict__ part,
                            uint64_t* __restrict__ support, uint2* tier0, uint2* tier1, uint2* tier2,
-                           uint2* bigq, uint32_t* vflag, uint32_t epoch, Counters* c) {
+                           uint2* bigq, uint32_t* vflag, uint32_t epoch, Counters* c, uint32_t hmax,
+                           uint32_t dlim) {
   __shared__ unsigned long long s_acc[8][32];  // launched with 256 threads
   const uint32_t ln = lane_id(), wib = threadIdx.x >> 5;
   unsigned long long* acc = s_acc[wib & 7];
@@ -194,7 +197,7 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
       if (MODE == 1 && work) work = support[u] != 0;
       if (work) {
         pb = pb64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb64;
-        tier = pb <= kWarpCap ? 0 : pb <= kCtaCap ? 1 : 2;
+        tier = pb <= kWarpCap ? 0 : (pb <= hmax && d < dlim) ? 1 : 2;
         wsum += s;
         ssum += d;
         tw[tier] += s;
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(512) k_classify_big(const uint2* __restrict__ 
                                                      const uint32_t* __restrict__ ld, uint64_t* __restrict__ support,
                                                      uint2* tier0, uint2* tier1, uint2* tier2, uint32_t* vflag,
                                                      uint32_t epoch,
-                                                     Counters* c) {
+                                                     Counters* c, uint32_t hmax, uint32_t dlim) {
   __shared__ unsigned long long s_part[16];
   const uint32_t n = cnt->nbig;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(512) k_classify_big(const uint2* __restrict__ 
       if (MODE == 1 && work) work = support[u] != 0;
       if (work) {
         const uint32_t pb = pb64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)pb64;
-        const int tier = pb <= kWarpCap ? 0 : pb <= kCtaSlots / 2 ? 1 : 2;
+        const int tier = pb <= kWarpCap ? 0 : (pb <= hmax && d < dlim) ? 1 : 2;
         uint2* tl = tier == 0 ? tier0 : tier == 1 ? tier1 : tier2;
         tl[atomicAdd(&c->ntier[tier], 1u)] = make_uint2(u, pb);
         atomicAdd(&c->wedges, s);
@@ -320,6 +323,13 @@ struct AggArgs {
   uint32_t* cc;                        // LINK: union-find parents (k-tip components)
   const uint32_t* __restrict__ cut_e;  // LINK: per U-edge (u, v), members of N_v with id < u
   uint32_t idspace;                    // tier-2 windows cover partner ids [0, idspace) (COUNT, PEEL)
+  // tier 1 (agg_hash.cuh): window-bound rows of long lists, degree-mass windows, count-field bits
+  const uint32_t* __restrict__ rowid;
+  const uint32_t* __restrict__ rows;
+  const uint32_t* __restrict__ wb;
+  uint32_t cb;
+  uint2* tier2;                        // starts tier 1 passes on (a window above its capacity)
+  uint32_t* ntier2;
 };
 
 // Partner lists of the aggregation tiers: the live prefix of N_v (COUNT, PEEL),
@@ -403,6 +413,7 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
 
 #include "agg_mid.cuh"
 #include "agg_win.cuh"
+#include "agg_hash.cuh"
 
 // ---------------------------------------------------------------- range pass
 // Partition start (Alg.4 l.5-8): snapshot ⋈^init = support for all
@@ -526,7 +537,7 @@ __global__ void __launch_bounds__(256) k_collect_touched(uint32_t nV, uint32_t* 
 // placed directly after the live prefix, so over the whole CD each N_v ends as
 // [U_last | ... | U_1] — grouped by partition, which is the induced-subgraph
 // layout FD needs.  Lists shorter than `big` use one warp,
-// longer ones one CTA (k_compact_big).
+// longer ones are chunked over CTAs (k_compact_plan / _count / _scan / _scatter).
 __global__ void k_compact(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv,
                           const uint64_t* __restrict__ offV, uint32_t* adjL, uint32_t* tmp, uint32_t* ld,
                           const uint32_t* __restrict__ part, uint32_t big, Counters* c) {
@@ -563,48 +574,6 @@ __global__ void k_compact(const uint32_t* __restrict__ tv, const uint32_t* __res
   }
   drop = warp_sum(drop);
   if (ln == 0 && drop) atomicAdd(&c->ld2_drop, drop);
-}
-
-__global__ void __launch_bounds__(512) k_compact_big(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv,
-                                                     const uint64_t* __restrict__ offV, uint32_t* adjL, uint32_t* tmp,
-                                                     uint32_t* ld, const uint32_t* __restrict__ part, uint32_t big,
-                                                     Counters* c) {
-  __shared__ uint32_t s_scan[33];
-  __shared__ uint32_t s_L;
-  const uint32_t n = *ntv;
-  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const uint32_t v = tv[i];
-    if (threadIdx.x == 0) s_L = ld[v];
-    __syncthreads();
-    const uint32_t L = s_L;
-    if (L < big) {
-      __syncthreads();
-      continue;
-    }
-    const uint64_t base = offV[v];
-    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) tmp[base + t] = adjL[base + t];
-    __syncthreads();
-    uint32_t lw = 0, dw = 0;
-    for (uint32_t t0 = 0; t0 < L; t0 += blockDim.x) {
-      const uint32_t t = t0 + threadIdx.x;
-      const bool ok = t < L;
-      const uint32_t x = ok ? tmp[base + t] : 0u;
-      const bool live = ok && part[x] == kUnassigned;
-      const bool dead = ok && !live;
-      uint32_t tl, td;
-      const uint32_t rl = block_excl_scan(live ? 1u : 0u, s_scan, &tl);
-      const uint32_t rd = block_excl_scan(dead ? 1u : 0u, s_scan, &td);
-      if (live) adjL[base + lw + rl] = x;
-      if (dead) adjL[base + L - 1 - (dw + rd)] = x;
-      lw += tl;
-      dw += td;
-    }
-    if (threadIdx.x == 0) {
-      ld[v] = lw;
-      atomicAdd(&c->ld2_drop, (unsigned long long)L * L - (unsigned long long)lw * lw);
-    }
-    __syncthreads();
-  }
 }
 
 // Lists of >= `big` entries are compacted by several CTAs: chunks of

@@ -33,6 +33,7 @@ struct VpULists {
     base = offV[v];
     len = cut[v];
   }
+  __device__ __forceinline__ uint32_t mid(uint64_t e) const { return adjU[e]; }
 };
 // start ∈ V: edge e of the start (live N_v) -> mid u, partner list = N_u prefix
 struct VpVLists {
@@ -108,7 +109,7 @@ struct VpSide<1> {  // start ∈ V
 // tier 1 (CTA).  A warp takes 32 starts and walks their edges flattened.
 template <int SIDE>
 __global__ void __launch_bounds__(256) k_vp_classify(uint32_t n, AggArgs a, uint2* tier0, uint2* tier1,
-                                                     uint2* tier2, uint2* bigq) {
+                                                     uint2* tier2, uint2* bigq, uint32_t hmax, uint32_t dlim) {
   __shared__ unsigned long long s_acc[8][32];
   const uint32_t ln = lane_id();
   unsigned long long* acc = s_acc[threadIdx.x >> 5];
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(256) k_vp_classify(uint32_t n, AggArgs a, uint
     uint32_t pb = 0;
     if (ok && mine) {
       pb = mine > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)mine;
-      tier = pb <= kWarpCap ? 0 : pb <= kCtaCap ? 1 : 2;
+      tier = pb <= kWarpCap ? 0 : (pb <= hmax && d < dlim) ? 1 : 2;
       wsum += mine;
       ssum += d;
     }
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(256) k_vp_classify(uint32_t n, AggArgs a, uint
 // The starts k_vp_classify deferred (more than kClassBig lists): one CTA each.
 template <int SIDE>
 __global__ void __launch_bounds__(512) k_vp_classify_big(AggArgs a, const uint2* __restrict__ bigq, uint2* tier0,
-                                                         uint2* tier1, uint2* tier2) {
+                                                         uint2* tier1, uint2* tier2, uint32_t hmax, uint32_t dlim) {
   __shared__ unsigned long long s_part[16];
   const uint32_t n = a.c->nbig;
   const auto L = VpSide<SIDE>::lists(a);
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(512) k_vp_classify_big(AggArgs a, const uint2*
       for (uint32_t w = 0; w < (blockDim.x >> 5); w++) s += s_part[w];
       if (s) {
         const uint32_t pb = s > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)s;
-        const int tier = pb <= kWarpCap ? 0 : pb <= kCtaCap ? 1 : 2;
+        const int tier = pb <= kWarpCap ? 0 : (pb <= hmax && e1 - e0 < dlim) ? 1 : 2;
         uint2* tl = tier == 0 ? tier0 : tier == 1 ? tier1 : tier2;
         tl[atomicAdd(&a.c->ntier[tier], 1u)] = make_uint2(x, pb);
         atomicAdd(&a.c->wedges, s);
@@ -359,6 +360,14 @@ __global__ void __launch_bounds__(kMidThreads, kMidCtas) k_vp_agg_mid(AggArgs a)
   }
 }
 
+// Tier 1 for starts in U: packed hash tables over degree-mass windows
+// (agg_hash.cuh); C(w,2) to every last below the start and to the start.
+__global__ void __launch_bounds__(kHashThreads, kHashCtas) k_vp_agg_hash(AggArgs a) {
+  extern __shared__ __align__(16) unsigned char hsm_[];
+  HashSmem& S = *reinterpret_cast<HashSmem*>(hsm_);
+  hash_tier<3>(a, VpSide<0>::lists(a), S);
+}
+
 // Tier 2: one CTA per start, window bitmap over segments (agg_win.cuh).
 template <int SIDE>
 __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_vp_agg_win(AggArgs a) {
@@ -392,14 +401,14 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_vp_agg_win(AggArgs a)
           acc += d;
         }
       };
-      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c->dbg, false);
+      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c, false);
       acc = warp_sum(acc);
       if (lane_id() == 0 && acc) atomicAdd(&sh.acc, (unsigned long long)acc);
       __syncthreads();
       if (threadIdx.x == 0 && sh.acc) red_add_u64(&a.support[x], sh.acc);
     } else {
       auto out = [&](uint32_t, uint32_t) {};
-      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c->dbg, false,
+      win_agg_one(L, e0, e1, 0xFFFFFFFFu, x, t % G, G, partner, S, sh, bnd, a.win_pre, out, a.c, false,
                   VpPass2{a.adjV, a.support});
     }
     __syncthreads();

@@ -54,18 +54,36 @@ size_t warp_tier_smem() { return (size_t)(kWarpTierThreads / 32) * 2 * kWarpSlot
 size_t mid_smem() { return sizeof(MidSmem); }
 size_t win_smem() { return sizeof(WinSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
+size_t hash_smem() { return sizeof(HashSmem); }
 size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kFdCtaSlots + kFdThreads) * 4; }
 
-void set_attrs_once() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    // keep stream-ordered scratch cached between calls (no re-mapping per decomposition)
-    int dev = 0;
+// Per-device one-time setup: the dynamic shared-memory opt-ins (they apply to
+// the current device only) and a private stream-ordered memory pool for the
+// library's scratch.  The pool keeps freed scratch mapped, inside a call and
+// between calls (re-mapping ~20 GB of config-5 scratch per call costs
+// hundreds of ms), until pbng_release_memory() trims it; the device's default
+// pool, which other allocators in the process share, is never reconfigured.
+constexpr int kMaxDevices = 64;
+std::mutex g_dev_mu;
+bool g_dev_ready[kMaxDevices];
+cudaMemPool_t g_dev_pool[kMaxDevices];
+
+cudaMemPool_t device_setup(int dev) {
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  if (dev < 0 || dev >= kMaxDevices) fail(PBNG_ERR_ARG, "device index out of range");
+  if (g_dev_ready[dev]) return g_dev_pool[dev];
+  {
+    cudaMemPoolProps props;
+    std::memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    CK(cudaMemPoolCreate(&pool, &props));
+    uint64_t thr = ~0ull;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_dev_pool[dev] = pool;
     cudaFuncSetAttribute(k_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_mid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
@@ -84,8 +102,14 @@ void set_attrs_once() {
     cudaFuncSetAttribute(k_range_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem());
     cudaFuncSetAttribute(k_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem());
     cudaFuncSetAttribute(k_fdg_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kGridCnt * 4));
-    cudaGetLastError();
-  });
+    CK(cudaFuncSetAttribute(k_agg_hash<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
+    CK(cudaFuncSetAttribute(k_agg_hash<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
+    CK(cudaFuncSetAttribute(k_agg_hash<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
+    CK(cudaFuncSetAttribute(k_vp_agg_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
+    CK(cudaGetLastError());
+  }
+  g_dev_ready[dev] = true;
+  return g_dev_pool[dev];
 }
 
 // Graph oriented so that U is the peel side (device pointers).
@@ -131,7 +155,7 @@ class Run {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    set_attrs_once();
+    pool = device_setup(dev);
     CK(cudaMallocHost(&hc, sizeof(Counters)));
   }
   ~Run() {
@@ -155,7 +179,7 @@ class Run {
   template <class T>
   T* alloc(size_t n) {
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, std::max<size_t>(n, 1) * sizeof(T), pool, st);
     if (e != cudaSuccess) {
       cudaGetLastError();
       fail(PBNG_ERR_OOM, "cudaMallocAsync of " + std::to_string(n * sizeof(T)) + " bytes failed: " +
@@ -200,6 +224,7 @@ class Run {
     return *hc;
   }
   cudaStream_t st;
+  cudaMemPool_t pool = nullptr;
   int nsm = 148;
   Counters* hc = nullptr;
   bool timing = false;
@@ -433,6 +458,15 @@ struct State {
   uint32_t* cc = nullptr;     // k-tip level retrieval: union-find parents
   uint32_t* cut_e = nullptr;  // ... and per U-edge partner-prefix lengths
   uint32_t idspace = 0;       // 1 + largest live id (tier-2 window range; ids above are all peeled)
+  // tier 1 (agg_hash.cuh): degree-mass windows, window-bound rows of long V lists
+  uint32_t* wb = nullptr;
+  uint32_t* rowid = nullptr;
+  uint32_t* rows = nullptr;
+  uint32_t cb = 0, dlim = 0;  // count-field bits of a packed slot; starts need fewer lists than dlim
+  // CD grid mode (agg_win.cuh): per-start dense counters for batches of few tier-2 starts
+  uint32_t* gcnt = nullptr;
+  uint64_t gcnt_cap = 0;
+  uint64_t grid_starts = 0;
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -493,6 +527,37 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank&
     k_vp_cut_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.offU, g.adjU, RV.binoff, RV.dmax, S.cutU);
     r.post(PBNG_K_COUNT_VP);
   }
+  // tier 1: packed slot = (x + 1) << cb | w, x + 1 <= nU needs bitlen(nU) key bits
+  const uint32_t keybits = g.nU ? 32u - (uint32_t)__builtin_clz(g.nU) : 1u;
+  S.cb = 32u - keybits;
+  S.dlim = S.cb >= 7 ? kHashLists : (1u << S.cb);
+  S.wb = r.alloc<uint32_t>(kHW + 1);
+  r.pre(PBNG_K_INIT);
+  k_mass_windows<<<1, 64, 0, r.st>>>(g.nU, g.m, g.offU, S.wb);
+  r.post(PBNG_K_INIT);
+  S.rowid = r.alloc<uint32_t>(g.nV);
+  uint32_t* nrows = r.alloc<uint32_t>(1);
+  CK(cudaMemsetAsync(nrows, 0, 4, r.st));
+  if (g.nV) {
+    r.pre(PBNG_K_INIT);
+    k_rows_ids<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, g.offV, S.rowid, nrows);
+    r.post(PBNG_K_INIT);
+  }
+  uint32_t hrows = 0;
+  CK(cudaMemcpyAsync(&hrows, nrows, 4, cudaMemcpyDeviceToHost, r.st));
+  CK(cudaStreamSynchronize(r.st));
+  S.rows = r.alloc<uint32_t>((size_t)hrows * (kHW + 1));
+  if (hrows) {
+    r.pre(PBNG_K_INIT);
+    k_rows_fill<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, nullptr, nullptr, S.rowid, g.offV, S.adjL, S.ld, S.wb, S.rows);
+    r.post(PBNG_K_INIT);
+  }
+  if (need_live) {
+    // grid mode counters: up to kGridStarts starts x live id range, zero between uses
+    S.gcnt_cap = std::min<uint64_t>((uint64_t)kGridStarts * g.nU, 256ull << 20);
+    S.gcnt = r.alloc<uint32_t>(S.gcnt_cap);
+    CK(cudaMemsetAsync(S.gcnt, 0, S.gcnt_cap * 4, r.st));
+  }
   const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWinIds - 1) / kWinIds;
   // per-CTA tables of starts with up to win_pre lists: bounds + chunk prefixes
   // ((W+1) u32 each per list) and list bases (u64); about 8 MB per CTA at most
@@ -525,11 +590,17 @@ AggArgs agg_args(const State& S, int t) {
   a.cc = S.cc;
   a.cut_e = S.cut_e;
   a.idspace = S.idspace;
+  a.rowid = S.rowid;
+  a.rows = S.rows;
+  a.wb = S.wb;
+  a.cb = S.cb;
+  a.tier2 = S.tier[2];
+  a.ntier2 = &S.c->ntier[2];
   return a;
 }
 
 template <int MODE>
-void launch_agg(Run& r, const State& S, const uint32_t* ntier) {
+void launch_agg(Run& r, State& S, const uint32_t* ntier, unsigned long long wedges = 0) {
   // ntier: tier sizes read back by the host (launch only non-empty tiers)
   if (ntier[0]) {
     r.pre(PBNG_K_AGG_WARP);
@@ -537,11 +608,31 @@ void launch_agg(Run& r, const State& S, const uint32_t* ntier) {
     r.post(PBNG_K_AGG_WARP);
   }
   if (ntier[1]) {
+    r.pre(PBNG_K_AGG_HASH);
+    k_agg_hash<MODE><<<r.nsm * kHashCtas, kHashThreads, hash_smem(), r.st>>>(agg_args(S, 1));
+    r.post(PBNG_K_AGG_HASH);
+  }
+  uint32_t first = 0;  // tier-2 starts handled by grid mode
+  // (the counters must fit, and stay L2-sized or small next to the batch's wedges)
+  const uint64_t cells = (uint64_t)ntier[2] * S.idspace;
+  if (MODE == 1 && S.gcnt && ntier[2] && ntier[2] <= kGridStarts && cells <= S.gcnt_cap &&
+      cells <= std::max<uint64_t>(16ull << 20, 2 * wedges)) {
+    // few tier-2 starts: every SM walks their lists into per-start dense counters
+    first = ntier[2];
+    S.grid_starts += first;
+    const CdLists L{S.g.adjU, S.g.offV, S.ld};
     r.pre(PBNG_K_AGG_CTA);
-    k_agg_mid<MODE><<<r.nsm * kMidCtas, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
+    k_grid_mark<<<r.nsm * 8, 256, 0, r.st>>>(S.tier[2], first, L, S.g.offU, S.adjL, S.idspace, S.gcnt);
+    r.post(PBNG_K_AGG_CTA);
+    r.pre(PBNG_K_AGG_CTA);
+    k_grid_sweep<<<r.nsm * 8, 256, 0, r.st>>>(first, S.idspace, S.gcnt, S.support, S.c);
+    r.post(PBNG_K_AGG_CTA);
+    // the bitmap tier takes only the starts tier 1 passes on after these
+    r.pre(PBNG_K_AGG_CTA);
+    k_set_u32<<<1, 1, 0, r.st>>>(&S.c->ticket[2], first * S.win_split);
     r.post(PBNG_K_AGG_CTA);
   }
-  if (ntier[2]) {
+  if ((ntier[2] > first) || ntier[1]) {  // tier 1 passes on starts with a window above its capacity
     r.pre(PBNG_K_AGG_CTA);
     k_agg_win<MODE><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
     r.post(PBNG_K_AGG_CTA);
@@ -572,28 +663,32 @@ void vp_count_live(Run& r, State& S) {
   // starts in U
   reset_tiers(r, S);
   r.pre(PBNG_K_CLASSIFY);
-  k_vp_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(g.nU, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2], S.tier[3]);
+  k_vp_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(g.nU, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2], S.tier[3],
+                                                 kHashMaxPb, S.dlim);
   r.post(PBNG_K_CLASSIFY);
   r.pre(PBNG_K_CLASSIFY);
-  k_vp_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(agg_args(S, 0), S.tier[3], S.tier[0], S.tier[1], S.tier[2]);
+  k_vp_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(agg_args(S, 0), S.tier[3], S.tier[0], S.tier[1], S.tier[2],
+                                                    kHashMaxPb, S.dlim);
   r.post(PBNG_K_CLASSIFY);
   S.win_split = pick_split(r, r.readback(S.c).ntier[2], g.nU);
   r.pre(PBNG_K_AGG_WARP);
   k_vp_agg_warp<0><<<r.nsm * 3, kWarpTierThreads, warp_tier_smem(), r.st>>>(agg_args(S, 0));
   r.post(PBNG_K_AGG_WARP);
-  r.pre(PBNG_K_AGG_CTA);
-  k_vp_agg_mid<0><<<r.nsm * kMidCtas, kMidThreads, mid_smem(), r.st>>>(agg_args(S, 1));
-  r.post(PBNG_K_AGG_CTA);
+  r.pre(PBNG_K_AGG_HASH);
+  k_vp_agg_hash<<<r.nsm * kHashCtas, kHashThreads, hash_smem(), r.st>>>(agg_args(S, 1));
+  r.post(PBNG_K_AGG_HASH);
   r.pre(PBNG_K_AGG_CTA);
   k_vp_agg_win<0><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
   r.post(PBNG_K_AGG_CTA);
   // starts in V
   reset_tiers(r, S);
   r.pre(PBNG_K_CLASSIFY);
-  k_vp_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(g.nV, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2], S.tier[3]);
+  k_vp_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(g.nV, agg_args(S, 0), S.tier[0], S.tier[1], S.tier[2], S.tier[3],
+                                                 kCtaCap, 0xFFFFFFFFu);
   r.post(PBNG_K_CLASSIFY);
   r.pre(PBNG_K_CLASSIFY);
-  k_vp_classify_big<1><<<r.nsm * 2, 512, 0, r.st>>>(agg_args(S, 0), S.tier[3], S.tier[0], S.tier[1], S.tier[2]);
+  k_vp_classify_big<1><<<r.nsm * 2, 512, 0, r.st>>>(agg_args(S, 0), S.tier[3], S.tier[0], S.tier[1], S.tier[2],
+                                                    kCtaCap, 0xFFFFFFFFu);
   r.post(PBNG_K_CLASSIFY);
   S.win_split = pick_split(r, r.readback(S.c).ntier[2], g.nV);
   r.pre(PBNG_K_AGG_WARP);
@@ -618,11 +713,11 @@ void count_live(Run& r, State& S) {
   r.pre(PBNG_K_CLASSIFY);
   k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(S.g.nU, nullptr, nullptr, S.g.offU, S.g.adjU, S.ld, S.part,
                                                S.support, S.tier[0], S.tier[1], S.tier[2], S.tier[3], nullptr, 0,
-                                               S.c);
+                                               S.c, kHashMaxPb, S.dlim);
   r.post(PBNG_K_CLASSIFY);
   r.pre(PBNG_K_CLASSIFY);
   k_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, S.g.offU, S.g.adjU, S.ld, S.support, S.tier[0],
-                                                  S.tier[1], S.tier[2], nullptr, 0, S.c);
+                                                  S.tier[1], S.tier[2], nullptr, 0, S.c, kHashMaxPb, S.dlim);
   r.post(PBNG_K_CLASSIFY);
   const Counters hc = r.readback(S.c);
   S.win_split = pick_split(r, hc.ntier[2], S.idspace);
@@ -658,6 +753,11 @@ void compact(Run& r, State& S, uint32_t epoch, bool force = false) {
   k_compact_scatter<<<r.nsm * 4, kCompThreads, 0, r.st>>>(S.comp_task, S.comp_ntask, S.touched, S.comp_oldL,
                                                           S.comp_tbase, S.comp_cnt, S.g.offV, S.ld, S.adjL, S.tmp,
                                                           S.part);
+  r.post(PBNG_K_COMPACT);
+  // window-bound rows of the compacted lists (tier 1)
+  r.pre(PBNG_K_COMPACT);
+  k_rows_fill<<<r.nsm * 8, 256, 0, r.st>>>(0, S.touched, &S.c->ntouched, S.rowid, S.g.offV, S.adjL, S.ld, S.wb,
+                                           S.rows);
   r.post(PBNG_K_COMPACT);
 }
 
@@ -742,11 +842,12 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
       r.pre(PBNG_K_CLASSIFY);
       k_classify<1><<<r.nsm * 8, 256, 0, r.st>>>(nU, S.F, &S.c->nF, S.g.offU, S.g.adjU, S.ld, S.part, S.support,
                                                    S.tier[0], S.tier[1], S.tier[2], S.tier[3], S.vflag, epoch,
-                                                   S.c);
+                                                   S.c, kHashMaxPb, S.dlim);
       r.post(PBNG_K_CLASSIFY);
       r.pre(PBNG_K_CLASSIFY);
       k_classify_big<1><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, S.g.offU, S.g.adjU, S.ld, S.support,
-                                                      S.tier[0], S.tier[1], S.tier[2], S.vflag, epoch, S.c);
+                                                      S.tier[0], S.tier[1], S.tier[2], S.vflag, epoch, S.c,
+                                                      kHashMaxPb, S.dlim);
       r.post(PBNG_K_CLASSIFY);
       const Counters hc = r.readback(S.c);
       if (hc.nF == 0) break;
@@ -772,7 +873,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         st.recounts++;
       } else {
         S.win_split = pick_split(r, hc.ntier[2], S.idspace);
-        launch_agg<1>(r, S, hc.ntier);
+        launch_agg<1>(r, S, hc.ntier, hc.wedges);
         if (del) compact(r, S, epoch);
       }
       if (trace) {
@@ -1051,7 +1152,9 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   const Counters c1 = r.readback(S.c);
   st.support_updates += c1.updates;
   st.wedges_cd = c1.cum_wedges - c0.cum_wedges;
-  for (int i = 0; i < 4; i++) st.impl[i] = c1.dbg[i];
+  for (int i = 0; i < 3; i++) st.impl[i] = c1.dbg[i];
+  st.impl[3] = S.grid_starts;
+  for (int i = 0; i < 4; i++) st.impl_hash[i] = c1.hashc[i];
   st.uv_steps += c1.cum_steps;
   st.ms_count = elapsed(t0, t1);
   st.ms_cd = elapsed(t1, t2);
@@ -1097,24 +1200,38 @@ uint32_t tip_level(const Dev& g, const uint64_t* tip, uint64_t k, uint32_t* out_
   uint32_t* minlab = r.alloc<uint32_t>(g.nU);
   uint32_t* dn = r.alloc<uint32_t>(1);
   CK(cudaMemsetAsync(dn, 0, 4, r.st));
+  r.pre(PBNG_K_INIT);
   k_level_mark<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, tip, k, S.part, S.cc, minlab);
+  r.post(PBNG_K_INIT);
   if (g.nV) {
     CK(cudaMemsetAsync(S.vflag, 1, (size_t)g.nV * 4, r.st));  // every list may hold non-members
     compact(r, S, 0, true);
   }
   S.cut_e = r.alloc<uint32_t>(std::max<uint64_t>(gr.m, 1));
-  if (gr.m)
+  if (gr.m) {
+    r.pre(PBNG_K_INIT);
     k_level_cut<<<r.nsm * 8, 256, 0, r.st>>>(gr.nU, gr.m, gr.offU, gr.adjU, gr.offV, S.adjL, S.ld, S.part, S.cut_e);
+    r.post(PBNG_K_INIT);
+  }
   reset_tiers(r, S);
+  r.pre(PBNG_K_CLASSIFY);
   k_classify<0><<<r.nsm * 8, 256, 0, r.st>>>(gr.nU, nullptr, nullptr, gr.offU, gr.adjU, S.ld, S.part, S.support,
-                                               S.tier[0], S.tier[1], S.tier[2], S.tier[3], nullptr, 0, S.c);
+                                               S.tier[0], S.tier[1], S.tier[2], S.tier[3], nullptr, 0, S.c,
+                                               kHashMaxPb, S.dlim);
+  r.post(PBNG_K_CLASSIFY);
+  r.pre(PBNG_K_CLASSIFY);
   k_classify_big<0><<<r.nsm * 2, 512, 0, r.st>>>(S.tier[3], S.c, gr.offU, gr.adjU, S.ld, S.support, S.tier[0],
-                                                  S.tier[1], S.tier[2], nullptr, 0, S.c);
+                                                  S.tier[1], S.tier[2], nullptr, 0, S.c, kHashMaxPb, S.dlim);
+  r.post(PBNG_K_CLASSIFY);
   const Counters hc = r.readback(S.c);
   S.win_split = pick_split(r, hc.ntier[2], gr.nU);
   launch_agg<2>(r, S, hc.ntier);
+  r.pre(PBNG_K_INIT);
   k_level_minlab<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.part, S.cc, minlab);
+  r.post(PBNG_K_INIT);
+  r.pre(PBNG_K_INIT);
   k_level_label<<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.part, S.cc, minlab, out_comp, dn);
+  r.post(PBNG_K_INIT);
   uint32_t n = 0;
   CK(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, r.st));
   CK(cudaStreamSynchronize(r.st));
@@ -1245,6 +1362,14 @@ int pbng_kernel_times(float* out_ms) {
       event_pool().push_back(sp.b);
     }
     deferred_spans().clear();
+  });
+}
+
+int pbng_release_memory(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    for (int d = 0; d < kMaxDevices; d++)
+      if (g_dev_ready[d]) CK(cudaMemPoolTrimTo(g_dev_pool[d], 0));
   });
 }
 

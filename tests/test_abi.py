@@ -46,7 +46,19 @@ def test_missing_library_fails_loudly(tmp_path):
         pbng._lib = old
 
 
-def test_struct_layouts_match_header():
-    assert ctypes.sizeof(pbng.Csr) == 32
-    assert ctypes.sizeof(pbng.Stats) == 4 * 8 + 4 * 4 + 4 * 4 + 3 * 8 + 8 + 4 * 8 + 16 * 4
-    assert pbng.MAX_P == 4096
+def test_struct_layouts_match_header(tmp_path):
+    """sizeof / offsetof of the ABI structs as gcc compiles include/pbng.h = the ctypes binding's."""
+    import subprocess
+    fields = [f for f, _ in pbng.Stats._fields_]
+    src = tmp_path / "lay.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pbng.h"\nint main(void){'
+                   'printf("%zu %zu", sizeof(pbng_csr), sizeof(pbng_stats));'
+                   + "".join(f'printf(" %zu", offsetof(pbng_stats, {f}));' for f in fields)
+                   + 'printf(" %u\\n", PBNG_MAX_P); return 0;}')
+    exe = tmp_path / "lay"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert vals[0] == ctypes.sizeof(pbng.Csr)
+    assert vals[1] == ctypes.sizeof(pbng.Stats)
+    assert vals[2:-1] == [getattr(pbng.Stats, f).offset for f in fields]
+    assert vals[-1] == pbng.MAX_P == 4096
