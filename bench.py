@@ -249,7 +249,11 @@ def roofline(stats_list, peaks):
     dominant = max(ms, key=ms.get) if ms else None
     W = sum(s["wedges_count"] + s["wedges_cd"] for s in stats_list)
     S = sum(s["uv_steps"] - s["uv_steps_fd"] for s in stats_list)
-    A = sum(s["support_updates"] - s["updates_fd"] for s in stats_list)
+    # A = CD support decrements that reached partners still live (A_live, impl[3] of the stats
+    # step); decrements to partners peeled in the same batch or not yet compacted away are
+    # harmless extra work and are not counted as useful bytes
+    A = sum(s["impl"][3] for s in stats_list)
+    A_all = sum(s["support_updates"] - s["updates_fd"] for s in stats_list)
     bytes_alg = 4 * W + 20 * S + 20 * A  # 4 B/wedge, 20 B/(u,v) step, 20 B/update
     achieved = bytes_alg / (agg_ms / 1000) / 1e9 if agg_ms else 0.0
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -270,7 +274,9 @@ def roofline(stats_list, peaks):
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_launch": traffic_note, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
             else "fallback 6650 GB/s (B200_PROFILING.md)",
-            "bytes_alg_per_step": bytes_alg / max(1, len(stats_list)), "agg_ms_per_step": agg_ms / max(1, len(stats_list)),
+            "bytes_alg_per_step": bytes_alg / max(1, len(stats_list)),
+            "terms": {"W_wedges": W, "S_uv_steps": S, "A_live_updates": A, "A_all_cd_updates": A_all,
+                      "formula": "4*W + 20*S + 20*A_live"}, "agg_ms_per_step": agg_ms / max(1, len(stats_list)),
             "dominant_family_by_time": dominant, "ms_by_family_per_step":
                 {k: v / max(1, len(stats_list)) for k, v in sorted(ms.items(), key=lambda kv: -kv[1])}}
 

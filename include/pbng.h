@@ -78,7 +78,8 @@ typedef struct {
   uint32_t launches;         /* kernels launched by this call */
   uint32_t pad;
   uint64_t impl[4];          /* implementation counters (tier-2 bitmap windows, repeat-table overflows,
-                                dense passes, CD starts aggregated in grid mode) */
+                                dense passes) and [3] = CD support decrements that reached partners still
+                                live (A_live; counted only with PBNG_OPT_STATS / PBNG_OPT_STATS_DEFER, else 0) */
   /* device time per kernel family, filled only with PBNG_OPT_STATS (CUDA events
    * recorded on `stream` around each launch): index by PBNG_K_* */
   float ms_kernel[16];

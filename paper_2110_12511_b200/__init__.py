@@ -90,8 +90,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             getattr(lib, f).restype = ctypes.c_int
         lib.pbng_kernel_times.argtypes = [ctypes.c_void_p]
         lib.pbng_kernel_times.restype = ctypes.c_int
-        lib.pbng_release_memory.argtypes = []
-        lib.pbng_release_memory.restype = ctypes.c_int
+        if hasattr(lib, "pbng_release_memory"):  # (older tuning builds lack it)
+            lib.pbng_release_memory.argtypes = []
+            lib.pbng_release_memory.restype = ctypes.c_int
         lib.pbng_last_error.restype = ctypes.c_char_p
         lib.pbng_last_error.argtypes = []
         lib.pbng_version.restype = ctypes.c_char_p

@@ -467,10 +467,7 @@ __device__ __forceinline__ void hash_tier(const AggArgs& a, const L& lists, Hash
     }
     __syncthreads();
   }
-  if (MODE == 1) {
-    upd = warp_sum(upd);
-    if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
-  }
+  if (MODE == 1) flush_updates(a, upd);
 }
 
 template <int MODE>

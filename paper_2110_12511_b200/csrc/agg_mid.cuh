@@ -129,8 +129,5 @@ __global__ void __launch_bounds__(kMidThreads, kMidCtas) k_agg_mid(AggArgs a) {
     }
     __syncthreads();
   }
-  if (MODE == 1) {
-    upd = warp_sum(upd);
-    if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
-  }
+  if (MODE == 1) flush_updates(a, upd);
 }

@@ -717,57 +717,5 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
     }
     __syncthreads();
   }
-  if (MODE == 1) {
-    upd = warp_sum(upd);
-    if (lane_id() == 0 && upd) atomicAdd(&a.c->updates, upd);
-  }
-}
-
-// ---------------------------------------------------------------- grid mode
-constexpr uint32_t kGridStarts = 64;  // batches with at most this many tier-2 starts use grid mode
-
-__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
-
-// CD peel of a batch with only a few tier-2 starts (the last partitions peel
-// the highest-degree vertices a handful at a time): one CTA per start (or per
-// window group) would leave most SMs idle while it walks up to ~10^5 lists.
-// Instead every SM walks a share of the starts' lists and counts w(s, x) in a
-// dense per-start array in global memory (L2-resident: the live id range is
-// small by then), then a sweep emits C(w,2) and zeroes the array again.  This
-// is the paper's private n-element wedge array, shared by the
-// whole GPU for one start.
-__global__ void __launch_bounds__(256) k_grid_mark(const uint2* __restrict__ list, uint32_t n2, CdLists L,
-                                                   const uint64_t* __restrict__ offU,
-                                                   const uint32_t* __restrict__ adjV, uint32_t idspace,
-                                                   uint32_t* __restrict__ cnt) {
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint32_t i = 0; i < n2; i++) {
-    const uint32_t u = list[i].x;
-    uint32_t* c = cnt + (uint64_t)i * idspace;
-    auto f = [&](bool ok, uint32_t x, uint64_t) {
-      if (ok && x != u && x < idspace) atomicAdd(&c[x], 1u);
-    };
-    const uint64_t e0 = offU[u], e1 = offU[u + 1];
-    for (uint64_t ch = e0 + gw * 32; ch < e1; ch += nw * 32)
-      warp_chunk(L, ch, ch + 32 < e1 ? ch + 32 : e1, adjV, 0xFFFFFFFFu, nullptr, nullptr, 0, f);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_grid_sweep(uint32_t n2, uint32_t idspace, uint32_t* __restrict__ cnt,
-                                                    uint64_t* support, Counters* c) {
-  unsigned long long upd = 0;
-  const uint64_t n = (uint64_t)n2 * idspace;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t w = cnt[j];
-    if (w) {
-      cnt[j] = 0u;
-      if (w >= 2) {
-        red_add_u64(&support[j % idspace], 0ull - choose2(w));
-        upd++;
-      }
-    }
-  }
-  upd = warp_sum(upd);
-  if (lane_id() == 0 && upd) atomicAdd(&c->updates, upd);
+  if (MODE == 1) flush_updates(a, upd);
 }

@@ -61,6 +61,7 @@ struct Counters {
   unsigned long long max_live;   // range pass: 1 + largest live id
   // cumulative
   unsigned long long updates;    // C(w,2) decrements
+  unsigned long long updates_live;  // ... of which to partners still live (counted with PBNG_OPT_STATS only)
   unsigned long long ld2_drop;   // compaction: decrease of Σ_v ld_v^2
   unsigned long long cum_wedges; // Σ of every classify's wedges
   unsigned long long cum_steps;  // Σ d_u of every traversed u ((u, v) steps)
@@ -330,6 +331,7 @@ struct AggArgs {
   uint32_t cb;
   uint2* tier2;                        // starts tier 1 passes on (a window above its capacity)
   uint32_t* ntier2;
+  bool stats;                          // PEEL: also count decrements to live partners (A_live)
 };
 
 // Partner lists of the aggregation tiers: the live prefix of N_v (COUNT, PEEL),
@@ -349,17 +351,31 @@ __device__ __forceinline__ void emit(const AggArgs& a, uint32_t u, uint32_t k, u
                                      unsigned long long& upd) {
   // PEEL skips the liveness test: a peeled partner's support is never read again
   // (selection, snapshots and FD only read live vertices), so decrementing it is
-  // harmless and saves a random load per emitted pair
+  // harmless and saves a random load per emitted pair.  With stats on, the
+  // decrements that reach live partners are counted separately (bits 36..63 of
+  // upd; flush_updates splits them): A_live of the roofline.
   if (w >= 2 && (MODE == 1 || a.part[k] == kUnassigned)) {
     const uint64_t d = choose2(w);
     if (MODE == 0) {
       acc += d;
     } else if (MODE == 1) {
       red_add_u64(&a.support[k], 0ull - d);
-      upd++;
+      upd += (a.stats && a.part[k] == kUnassigned) ? (1ull << 36) + 1ull : 1ull;
     } else {
       cc_union(a.cc, u, k);  // u and k share a butterfly inside the level
     }
+  }
+}
+
+// Per-thread update counts -> Counters (whole warp, converged): low 36 bits all
+// decrements, high 28 bits the live ones; the fields are summed separately over
+// the warp, so the split is exact while one thread's totals in one launch stay
+// below 2^36 / 2^28 (a CD launch emits ~10^9 decrements over ~10^5 threads).
+__device__ __forceinline__ void flush_updates(const AggArgs& a, unsigned long long upd) {
+  const unsigned long long all = warp_sum(upd & ((1ull << 36) - 1)), live = warp_sum(upd >> 36);
+  if (lane_id() == 0) {
+    if (all) atomicAdd(&a.c->updates, all);
+    if (live) atomicAdd(&a.c->updates_live, live);
   }
 }
 
@@ -405,10 +421,7 @@ __global__ void __launch_bounds__(kWarpTierThreads) k_agg_warp(AggArgs a) {
     }
     __syncwarp();
   }
-  if (MODE == 1) {
-    upd = warp_sum(upd);
-    if (ln == 0 && upd) atomicAdd(&a.c->updates, upd);
-  }
+  if (MODE == 1) flush_updates(a, upd);
 }
 
 #include "agg_mid.cuh"

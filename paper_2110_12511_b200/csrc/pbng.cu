@@ -463,10 +463,7 @@ struct State {
   uint32_t* rowid = nullptr;
   uint32_t* rows = nullptr;
   uint32_t cb = 0, dlim = 0;  // count-field bits of a packed slot; starts need fewer lists than dlim
-  // CD grid mode (agg_win.cuh): per-start dense counters for batches of few tier-2 starts
-  uint32_t* gcnt = nullptr;
-  uint64_t gcnt_cap = 0;
-  uint64_t grid_starts = 0;
+  bool stats = false;         // count live-partner decrements (PBNG_OPT_STATS / _DEFER)
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -552,12 +549,6 @@ void alloc_state(Run& r, State& S, const Dev& g, bool need_live, const SideRank&
     k_rows_fill<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, nullptr, nullptr, S.rowid, g.offV, S.adjL, S.ld, S.wb, S.rows);
     r.post(PBNG_K_INIT);
   }
-  if (need_live) {
-    // grid mode counters: up to kGridStarts starts x live id range, zero between uses
-    S.gcnt_cap = std::min<uint64_t>((uint64_t)kGridStarts * g.nU, 256ull << 20);
-    S.gcnt = r.alloc<uint32_t>(S.gcnt_cap);
-    CK(cudaMemsetAsync(S.gcnt, 0, S.gcnt_cap * 4, r.st));
-  }
   const uint64_t wmax = ((uint64_t)std::max(g.nU, g.nV) + kWinIds - 1) / kWinIds;
   // per-CTA tables of starts with up to win_pre lists: bounds + chunk prefixes
   // ((W+1) u32 each per list) and list bases (u64); about 8 MB per CTA at most
@@ -596,11 +587,12 @@ AggArgs agg_args(const State& S, int t) {
   a.cb = S.cb;
   a.tier2 = S.tier[2];
   a.ntier2 = &S.c->ntier[2];
+  a.stats = S.stats;
   return a;
 }
 
 template <int MODE>
-void launch_agg(Run& r, State& S, const uint32_t* ntier, unsigned long long wedges = 0) {
+void launch_agg(Run& r, State& S, const uint32_t* ntier) {
   // ntier: tier sizes read back by the host (launch only non-empty tiers)
   if (ntier[0]) {
     r.pre(PBNG_K_AGG_WARP);
@@ -612,27 +604,7 @@ void launch_agg(Run& r, State& S, const uint32_t* ntier, unsigned long long wedg
     k_agg_hash<MODE><<<r.nsm * kHashCtas, kHashThreads, hash_smem(), r.st>>>(agg_args(S, 1));
     r.post(PBNG_K_AGG_HASH);
   }
-  uint32_t first = 0;  // tier-2 starts handled by grid mode
-  // (the counters must fit, and stay L2-sized or small next to the batch's wedges)
-  const uint64_t cells = (uint64_t)ntier[2] * S.idspace;
-  if (MODE == 1 && S.gcnt && ntier[2] && ntier[2] <= kGridStarts && cells <= S.gcnt_cap &&
-      cells <= std::max<uint64_t>(16ull << 20, 2 * wedges)) {
-    // few tier-2 starts: every SM walks their lists into per-start dense counters
-    first = ntier[2];
-    S.grid_starts += first;
-    const CdLists L{S.g.adjU, S.g.offV, S.ld};
-    r.pre(PBNG_K_AGG_CTA);
-    k_grid_mark<<<r.nsm * 8, 256, 0, r.st>>>(S.tier[2], first, L, S.g.offU, S.adjL, S.idspace, S.gcnt);
-    r.post(PBNG_K_AGG_CTA);
-    r.pre(PBNG_K_AGG_CTA);
-    k_grid_sweep<<<r.nsm * 8, 256, 0, r.st>>>(first, S.idspace, S.gcnt, S.support, S.c);
-    r.post(PBNG_K_AGG_CTA);
-    // the bitmap tier takes only the starts tier 1 passes on after these
-    r.pre(PBNG_K_AGG_CTA);
-    k_set_u32<<<1, 1, 0, r.st>>>(&S.c->ticket[2], first * S.win_split);
-    r.post(PBNG_K_AGG_CTA);
-  }
-  if ((ntier[2] > first) || ntier[1]) {  // tier 1 passes on starts with a window above its capacity
+  if (ntier[2] || ntier[1]) {  // tier 1 passes on starts with a window above its capacity
     r.pre(PBNG_K_AGG_CTA);
     k_agg_win<MODE><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
     r.post(PBNG_K_AGG_CTA);
@@ -873,7 +845,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         st.recounts++;
       } else {
         S.win_split = pick_split(r, hc.ntier[2], S.idspace);
-        launch_agg<1>(r, S, hc.ntier, hc.wedges);
+        launch_agg<1>(r, S, hc.ntier);
         if (del) compact(r, S, epoch);
       }
       if (trace) {
@@ -1137,6 +1109,7 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
     return;
   }
   State S;
+  S.stats = r.timing;
   cudaEvent_t t0 = r.event();
   SideRank RU, RV;
   const Dev gr = relabel(r, g, RU, RV);
@@ -1151,9 +1124,9 @@ void decompose(const Dev& g, uint32_t P, uint32_t opts, const Out& out, pbng_sta
   st.partitions_used = plan.nparts;
   const Counters c1 = r.readback(S.c);
   st.support_updates += c1.updates;
+  st.impl[3] = c1.updates_live;
   st.wedges_cd = c1.cum_wedges - c0.cum_wedges;
   for (int i = 0; i < 3; i++) st.impl[i] = c1.dbg[i];
-  st.impl[3] = S.grid_starts;
   for (int i = 0; i < 4; i++) st.impl_hash[i] = c1.hashc[i];
   st.uv_steps += c1.cum_steps;
   st.ms_count = elapsed(t0, t1);

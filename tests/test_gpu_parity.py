@@ -214,18 +214,19 @@ def _sample_levels(th, rng, k=64, max_members=2000):
 
 
 def test_config4_full_certificate(pb):
-    """Config 4 at full size (8M x 3M peel orientation, 30M edges, P=150):
-    sampled butterfly counts against the oracle, and the multi-core exactness
-    certificate (oracle/certificate.c) over every vertex and level."""
+    """Config 4 at full size (8M x 3M peel orientation, 30M edges, P=150): every
+    butterfly count equal to the oracle's, and the multi-core exactness certificate
+    (oracle/certificate.c) over every vertex and every level — one pass
+    over the unordered pairs gives the oracle counts and the (A) sums together."""
     g, P = gg.config(4)
     d = dev(pb, g)
     th = pb.as_u64(pb.pbng_tip_decompose(d, P)[0])
     sup = pb.as_u64(pb.pbng_count_butterflies(d))
-    rng = np.random.default_rng(44)
-    us = np.sort(rng.choice(g.nU, 20000, replace=False)).astype(np.uint32)
-    assert np.array_equal(sup[us], oracle.count_subset(g, us))
+    osup, sge, bad, first = oracle.cert_one_pass(g, th)
+    assert np.array_equal(sup, osup), "config 4 butterfly counts differ from the oracle"
     assert np.all(th <= sup)
-    assert oracle.certify(g, th)
+    assert np.all(sge >= th), "certificate (A) fails"
+    assert bad == 0, ("certificate (C) fails at level", first)
 
 
 def test_config5_sampled_certificate(pb):

@@ -4,8 +4,7 @@ the product kernels actually ran (implementation counters in pbng_stats):
   * tier-1 hash: starts split into id-window groups (impl_hash[1]) and starts passed on to
     the bitmap tier (impl_hash[3]);
   * tier-2 bitmap windows (impl[0]), repeat-table overflow -> dense recount (impl[1]),
-    dense windows (impl[2]);
-  * CD grid mode for batches of few tier-2 starts (impl[3]).
+    dense windows (impl[2]).
 The product build uses the same source with larger constants."""
 import json
 import os
@@ -37,4 +36,4 @@ def test_small_tables_every_path(cuda_ok):
     tot = _run("small", SMALL)
     impl, hsh = tot["impl"], tot["impl_hash"]
     assert hsh[0] > 0 and hsh[1] > 0 and hsh[2] > hsh[1] and hsh[3] > 0, hsh
-    assert impl[0] > 0 and impl[1] > 0 and impl[2] > 0 and impl[3] > 0, impl
+    assert impl[0] > 0 and impl[1] > 0 and impl[2] > 0, impl
