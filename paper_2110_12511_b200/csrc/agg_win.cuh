@@ -41,10 +41,10 @@ constexpr uint32_t kWinLogDup = PBNG_WIN_LOG_DUP;
 constexpr uint32_t kWinDupSlots = 1u << kWinLogDup;   // repeat table (key << 32 | repeats)
 constexpr uint32_t kWinDupCap = kWinDupSlots / 2;
 #ifndef PBNG_WIN_CHUNK
-#define PBNG_WIN_CHUNK 128
+#define PBNG_WIN_CHUNK 256
 #endif
 #ifndef PBNG_SEG_DEPTH
-#define PBNG_SEG_DEPTH 1
+#define PBNG_SEG_DEPTH 2
 #endif
 constexpr int kSegDepth = PBNG_SEG_DEPTH;  // 16-byte loads per lane issued together
 #ifndef PBNG_DENSE_DEPTH
@@ -388,9 +388,27 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   unsigned long long* prof_clk = cnt->prof;  // PBNG_TRACE phase clocks: [1] tables, [2] bitmap, [3] dense
   const uint32_t tid = threadIdx.x, bd = blockDim.x, ln = lane_id(), wid = tid >> 5, nw = bd >> 5;
   const uint64_t nl = e1 - e0;
-  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
-  const uint32_t k0 = (uint32_t)((uint64_t)g * W / G), k1 = (uint32_t)((uint64_t)(g + 1) * W / G);
-  if (k0 >= k1) return;
+  // id range [lo, hi) of this unit: whole coarse windows when the start is split
+  // into at most as many groups as it has windows, else equal id ranges (small
+  // batches of heavy starts, so that every SM has work)
+  uint64_t lo, hi;
+  {
+    const uint32_t Wall = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
+    if (G <= Wall) {
+      lo = (uint64_t)g * Wall / G * kWinIds;
+      hi = (uint64_t)(g + 1) * Wall / G * kWinIds;
+    } else {
+      const uint64_t span = (((uint64_t)idspace + G - 1) / G + 31) & ~31ull;
+      lo = (uint64_t)g * span;
+      hi = lo + span;
+    }
+    lo = lo < idspace ? lo : idspace;
+    hi = hi < idspace ? hi : idspace;
+  }
+  if (lo >= hi) return;
+  // windows k in [0, W): ids [lo + k * kWinIds, min(lo + (k + 1) * kWinIds, hi))
+  const uint32_t W = (uint32_t)((hi - lo + kWinIds - 1) / kWinIds);
+  const uint32_t k0 = 0, k1 = W;
   // fast path: every list's window bounds, base and per-window chunk prefixes
   // are computed once per start (per-CTA scratch), so a window needs no scan
   const uint32_t PL = pre_lists;  // scratch stride (lists) of the precomputed tables
@@ -404,7 +422,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   for (uint32_t k = tid; k < kWinMaxW; k += bd) S.ek[k] = 0;
   __syncthreads();
   if (pre) {
-    // bnd[i * (W + 1) + k] = first entry of list i with id >= min(k * kWinIds, idspace)
+    // bnd[i * (W + 1) + k] = first entry of list i with id >= min(lo + k * kWinIds, hi)
     for (uint32_t i = wid; i < nl; i += nw) {
       uint64_t base;
       uint32_t len;
@@ -415,8 +433,8 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         const uint32_t x = ln < len ? partner[base + ln] : 0xFFFFFFFFu;
         uint32_t prev = 0;
         for (uint32_t k = k0; k <= k1; k++) {
-          const uint64_t key = (uint64_t)k * kWinIds;
-          const uint32_t kk = key < idspace ? (uint32_t)key : idspace;
+          const uint64_t key = lo + (uint64_t)k * kWinIds;
+          const uint32_t kk = key < hi ? (uint32_t)key : (uint32_t)hi;
           const uint32_t v = __popc(__ballot_sync(kFull, x < kk));
           if (ln == 0) {
             bnd[(uint64_t)i * W1 + k] = v;
@@ -431,8 +449,8 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         const uint32_t k = kb + ln;
         uint32_t v = 0;
         if (k <= k1) {
-          const uint64_t key = (uint64_t)k * kWinIds;
-          v = lb_range(partner + base, 0, len, key < idspace ? (uint32_t)key : idspace);
+          const uint64_t key = lo + (uint64_t)k * kWinIds;
+          v = lb_range(partner + base, 0, len, key < hi ? (uint32_t)key : (uint32_t)hi);
           bnd[(uint64_t)i * W1 + k] = v;
         }
         uint32_t left = __shfl_up_sync(kFull, v, 1);
@@ -478,8 +496,8 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   __syncthreads();
   if (prof && tid == 0) atomicAdd(&prof_clk[1], (unsigned long long)(clock64() - tp0));
   for (uint32_t k = k0; k < k1; k++) {
-    const uint64_t wa = (uint64_t)k * kWinIds;
-    const uint64_t wb = wa + kWinIds < idspace ? wa + kWinIds : idspace;
+    const uint64_t wa = lo + (uint64_t)k * kWinIds;
+    const uint64_t wb = wa + kWinIds < hi ? wa + kWinIds : hi;
     const uint32_t kr = k - k0;
     bool dense = pre && S.ek[kr] > kDenseEntries;
     if (pre && S.ek[kr] == 0) continue;
@@ -516,10 +534,11 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         }
       };
       const long long tm0 = clock64();
+      // kSegDepth 16-byte loads per lane in flight per warp step (chunk = 128 * kSegDepth entries: one step)
       if (wch > kWinChunk)
-        run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<2>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
+        run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<2 * kSegDepth>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       else
-        run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<1>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
+        run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<kSegDepth>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       __syncthreads();
       const long long tm1 = clock64();
       if (prof && tid == 0) atomicAdd(&prof_clk[2], (unsigned long long)(tm1 - tm0));

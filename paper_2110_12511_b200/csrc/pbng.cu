@@ -615,13 +615,19 @@ void reset_tiers(Run& r, State& S) {
   CK(cudaMemsetAsync(&S.c->ntier[0], 0, 8 * sizeof(uint32_t), r.st));  // ntier[3] + ticket[4] + nbig
 }
 
-// Tier-2 starts are split into window groups when a batch has fewer than two
-// starts per SM, so that small batches still occupy every SM.
-uint32_t pick_split(const Run& r, uint32_t n2, uint32_t idspace) {
-  const uint32_t W = (uint32_t)(((uint64_t)idspace + kWinIds - 1) / kWinIds);
-  if (n2 == 0 || W <= 1) return 1;
-  const uint32_t want = (2u * (uint32_t)r.nsm * kWinCtas + n2 - 1) / n2;
-  return std::max(1u, std::min(want, W));
+// Tier-2 starts are split into units (groups of coarse windows, or equal id
+// ranges of at least kMinSpan ids when a start has fewer windows than the
+// split wants) when a batch has fewer than two starts per SM, so that small
+// batches of heavy starts still occupy every SM.  A unit should carry about
+// kMinUnitWedges wedges or more (wedges = the batch's classified wedges).
+constexpr uint64_t kMinSpan = 16384;
+constexpr uint64_t kMinUnitWedges = 1u << 16;
+uint32_t pick_split(const Run& r, uint32_t n2, uint32_t idspace, uint64_t wedges = ~0ull) {
+  if (n2 == 0 || idspace <= kMinSpan) return 1;
+  const uint64_t want = (2ull * (uint64_t)r.nsm * kWinCtas + n2 - 1) / n2;
+  const uint64_t by_ids = ((uint64_t)idspace + kMinSpan - 1) / kMinSpan;
+  const uint64_t by_work = std::max<uint64_t>(1, wedges / n2 / kMinUnitWedges);
+  return (uint32_t)std::max<uint64_t>(1, std::min({want, by_ids, by_work}));
 }
 
 // Vertex-priority count (Alg.1, kernels_vp.cuh) of every unassigned u on the
@@ -844,7 +850,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         count_live(r, S);
         st.recounts++;
       } else {
-        S.win_split = pick_split(r, hc.ntier[2], S.idspace);
+        S.win_split = pick_split(r, hc.ntier[2], S.idspace, hc.wedges);
         launch_agg<1>(r, S, hc.ntier);
         if (del) compact(r, S, epoch);
       }
