@@ -23,6 +23,9 @@
 #ifndef PBNG_WIN_LOG_IDS
 #define PBNG_WIN_LOG_IDS 20
 #endif
+#ifndef PBNG_WIN_MAX_W
+#define PBNG_WIN_MAX_W 64
+#endif
 #ifndef PBNG_WIN_THREADS
 #define PBNG_WIN_THREADS 1024
 #endif
@@ -94,8 +97,8 @@ struct WinSmem {
   uint32_t segT[kWinLists];
   unsigned long long segB[kWinLists]; // partner-array base of each list of the batch
   uint32_t scan[33];
-  unsigned long long ek[64];          // entries per coarse window (relative to the first window, kWinMaxW)
-  uint32_t ctot[64];                  // chunks per coarse window (fast path)
+  unsigned long long ek[PBNG_WIN_MAX_W];  // entries per coarse window (relative to the first window, kWinMaxW)
+  uint32_t ctot[PBNG_WIN_MAX_W];          // chunks per coarse window (fast path)
 };
 
 struct WinShared {
@@ -317,7 +320,7 @@ constexpr uint32_t kDenseIds = kWinBitWords * 2;
 #define PBNG_DENSE_ENTRIES 65536
 #endif
 constexpr uint64_t kDenseEntries = PBNG_DENSE_ENTRIES;  // coarse windows with more entries go dense
-constexpr uint32_t kWinMaxW = 64;              // windows whose entry counts are kept in shared memory
+constexpr uint32_t kWinMaxW = PBNG_WIN_MAX_W;  // windows whose entry counts are kept in shared memory
 
 // Dense marking: one atomicAdd per wedge; the first increment of a word
 // appends the word to the touched list (kept in the repeat table's memory,

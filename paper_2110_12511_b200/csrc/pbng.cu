@@ -620,7 +620,10 @@ void reset_tiers(Run& r, State& S) {
 // split wants) when a batch has fewer than two starts per SM, so that small
 // batches of heavy starts still occupy every SM.  A unit should carry about
 // kMinUnitWedges wedges or more (wedges = the batch's classified wedges).
-constexpr uint64_t kMinSpan = 16384;
+#ifndef PBNG_MIN_SPAN
+#define PBNG_MIN_SPAN 16384
+#endif
+constexpr uint64_t kMinSpan = PBNG_MIN_SPAN;
 constexpr uint64_t kMinUnitWedges = 1u << 16;
 uint32_t pick_split(const Run& r, uint32_t n2, uint32_t idspace, uint64_t wedges = ~0ull) {
   if (n2 == 0 || idspace <= kMinSpan) return 1;
@@ -749,7 +752,8 @@ struct TraceRow {
   uint32_t pid, nF, t0, t1, t2;
   unsigned long long wedges, w2cum;  // batch wedges; cumulative tier-2 wedges after classify
   bool recount;
-  cudaEvent_t a, b;
+  uint32_t idspace, split;
+  cudaEvent_t a, m, b;
 };
 
 void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats& st) {
@@ -843,7 +847,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
       const unsigned long long recount_cost = S.vp ? sums[1] : sums[0] - hc.ld2_drop;
       const bool recount = !(opts & PBNG_OPT_NO_RECOUNT) &&
                            ((opts & PBNG_OPT_FORCE_RECOUNT) || hc.wedges > recount_cost);
-      cudaEvent_t ta = trace ? r.event() : nullptr;
+      cudaEvent_t ta = trace ? r.event() : nullptr, tm = nullptr;
       if (recount) {
         // §5.1: re-compute supports of all remaining vertices
         if (del) compact(r, S, epoch);
@@ -852,11 +856,12 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
       } else {
         S.win_split = pick_split(r, hc.ntier[2], S.idspace, hc.wedges);
         launch_agg<1>(r, S, hc.ntier);
+        if (trace) tm = r.event();
         if (del) compact(r, S, epoch);
       }
       if (trace) {
-        TraceRow row{pid, hc.nF, hc.ntier[0], hc.ntier[1], hc.ntier[2], hc.wedges, hc.tier_wedges[2], recount, ta,
-                     r.event()};
+        TraceRow row{pid, hc.nF, hc.ntier[0], hc.ntier[1], hc.ntier[2], hc.wedges, hc.tier_wedges[2], recount,
+                     S.idspace, S.win_split, ta, tm ? tm : ta, r.event()};
         rows.push_back(row);
       }
     }
@@ -871,8 +876,9 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
                  "n_untabled=%llu n_tabled=%llu | windows=%llu over=%llu dense_passes=%llu\n", hc.prof[0], hc.prof[1],
                  hc.prof[2], hc.prof[3], hc.prof2[0], hc.prof2[1], hc.prof2[2], hc.dbg[0], hc.dbg[1], hc.dbg[2]);
     for (const TraceRow& t : rows)
-      std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu w2cum=%llu recount=%d ms=%.3f\n", t.pid,
-                   t.nF, t.t0, t.t1, t.t2, t.wedges, t.w2cum, (int)t.recount, elapsed(t.a, t.b));
+      std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu w2cum=%llu recount=%d ms=%.3f agg_ms=%.3f "
+                   "idspace=%u split=%u\n", t.pid, t.nF, t.t0, t.t1, t.t2, t.wedges, t.w2cum, (int)t.recount,
+                   elapsed(t.a, t.b), elapsed(t.a, t.m), t.idspace, t.split);
   }
 }
 
