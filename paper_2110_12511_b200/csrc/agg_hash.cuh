@@ -83,7 +83,8 @@ __device__ __forceinline__ bool hash_count(uint32_t* tab, uint32_t TB, uint32_t 
   const uint32_t kx = x + 1u, key = kx << cb;
   uint32_t b = __umulhi(x * 0x9E3779B1u, TB);
   const uint4* tab4 = reinterpret_cast<const uint4*>(tab);
-  for (;;) {
+  for (uint32_t probes = 0;; probes++) {
+    PBNG_DCHECK(probes <= TB);  // load <= 1/2: a free slot always exists
     const uint4 q = tab4[b];
     const uint32_t v[4] = {q.x, q.y, q.z, q.w};
     int hit = -1, emp = -1;
@@ -388,6 +389,7 @@ __device__ __forceinline__ bool hash_agg_one(const L& lists, uint64_t e0, uint64
         if (ok[j]) {
           uint32_t lo = l0;  // list lo: pre[lo] <= p < pre[lo + 1]
           while (S.pre[lo + 1] <= p) lo++;
+          PBNG_DCHECK(lo < d && lo != hl && S.seg0[lo] + (p - S.pre[lo]) < S.llen[lo]);
           x[j] = partner[S.lbase[lo] + S.seg0[lo] + (p - S.pre[lo])];
         }
       }

@@ -206,6 +206,7 @@ __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_
   auto one = [&](bool ok, uint32_t x) {
     const bool act = ok && x != skip;
     const uint32_t o = x - a;
+    PBNG_DCHECK(!act || o < kWinIds);  // the entry lies in the window
     const uint32_t bit = 1u << (o & 31);
     if (PBNG_COMBINE) {
       const uint32_t wd = act ? o >> 5 : 0xFFFFFFFFu;
@@ -340,6 +341,7 @@ __device__ __forceinline__ void dense_mark(const uint32_t* __restrict__ p, uint6
     uint32_t wd = 0;
     const bool act = ok && x != skip;
     const uint32_t o = x - a;
+    PBNG_DCHECK(!act || (o >> lf) < kWinBitWords);  // the entry lies in the dense sub-window
     const uint32_t inc = 1u << ((o & ((1u << lf) - 1)) << lb);
     if (PBNG_COMBINE_DENSE) {
       wd = act ? o >> lf : 0xFFFFFFFFu;
@@ -631,9 +633,21 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       const uint64_t b = a + SW < wb ? a + SW : wb;
       uint32_t* touch = reinterpret_cast<uint32_t*>(S.dup);
       if (tid == 0) sh.ndup = 0;  // touched-word count
+      const uint32_t fpw = 1u << (5 - lb);  // fields per word
+      const uint32_t nwords = (uint32_t)((b - a + fpw - 1) / fpw);
+      // Replicas: when the sub-window's counters fill only part of the array
+      // (late partitions: a few hundred live ids, millions of wedges per start),
+      // warps count into R copies (warp w into copy w mod R) so that they do not
+      // serialise on the same shared words; the sweep adds the copies (field-wise:
+      // every copy's field is at most the total, which the field width holds).
+      const uint32_t stride = (nwords + 3) & ~3u;
+      uint32_t R = 1;
+      if (!Pass2::kOn && !PBNG_DENSE_TOUCH)
+        while (2 * R <= 32 && 2 * R * stride <= kWinBitWords) R *= 2;
+      uint32_t* mycnt = S.bits + (wid & (R - 1)) * stride;
       __syncthreads();
       auto mark = [&](uint64_t i0, uint64_t i1, uint64_t) {
-        dense_mark(partner, i0, i1, (uint32_t)a, skip, lb, S.bits, touch, &sh.ndup);
+        dense_mark(partner, i0, i1, (uint32_t)a, skip, lb, mycnt, touch, &sh.ndup);
       };
       const uint32_t chunk = PBNG_DENSE_CHUNK ? PBNG_DENSE_CHUNK : (pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk);
       const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk, sub, sj, 33);
@@ -650,8 +664,6 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         };
         win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, sum, chunk, sub, sj, 33);
       }
-      const uint32_t fpw = 1u << (5 - lb);  // fields per word
-      const uint32_t nwords = (uint32_t)((b - a + fpw - 1) / fpw);
       const uint32_t nt = sh.ndup;
       const bool listed = PBNG_DENSE_TOUCH && nt <= kTouchCap;
       // fields with count >= 2 have a bit above their lowest bit set: find them
@@ -680,7 +692,17 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       } else {
         uint4* b4 = reinterpret_cast<uint4*>(S.bits);
         for (uint32_t t = tid; t < (nwords + 3) >> 2; t += bd) {
-          const uint4 v = b4[t];
+          uint4 v = b4[t];
+          for (uint32_t r = 1; r < R; r++) {
+            const uint4 y = b4[r * (stride >> 2) + t];
+            if (y.x | y.y | y.z | y.w) {
+              b4[r * (stride >> 2) + t] = make_uint4(0, 0, 0, 0);
+              v.x += y.x;
+              v.y += y.y;
+              v.z += y.z;
+              v.w += y.w;
+            }
+          }
           if (v.x | v.y | v.z | v.w) {
             b4[t] = make_uint4(0, 0, 0, 0);
             sweep_word(4 * t, v.x);

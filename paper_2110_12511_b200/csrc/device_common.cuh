@@ -5,6 +5,22 @@
 
 namespace pbng {
 
+// Checked builds (-DPBNG_CHECK=1, tests/test_gpu_checked.py): PBNG_DCHECK(c)
+// records the source line of the first failed condition in g_check_line
+// (no trap: the kernel runs on, the host turns the record into an error after
+// the call).  Stands in for compute-sanitizer memcheck, which this pool does
+// not allow: the checks guard the shared-memory table / bitmap indices, the
+// partner and support indices of every emitted update, and the list bounds of
+// compaction and FD.  Compiled out (constant false) in the product build.
+#ifndef PBNG_CHECK
+#define PBNG_CHECK 0
+#endif
+__device__ unsigned int g_check_line;
+#define PBNG_DCHECK(c)                                                       \
+  do {                                                                       \
+    if (PBNG_CHECK && !(c)) atomicCAS(&::pbng::g_check_line, 0u, (unsigned)__LINE__); \
+  } while (0)
+
 constexpr uint32_t kUnassigned = 0xFFFFFFFFu;  // part[u] of a vertex not yet peeled
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;       // empty hash key
 constexpr unsigned kFull = 0xFFFFFFFFu;
@@ -64,7 +80,8 @@ __device__ __forceinline__ void warp_append2(bool pred, uint2 val, uint2* list, 
 __device__ __forceinline__ void hash_insert(uint32_t* keys, uint32_t* vals, uint32_t logT, uint32_t k) {
   const uint32_t mask = (1u << logT) - 1;
   uint32_t h = (k * 0x9E3779B1u) >> (32 - logT);
-  for (;;) {
+  for (uint32_t probes = 0;; probes++) {
+    PBNG_DCHECK(probes <= mask);  // the table is never full
     uint32_t cur = ((volatile uint32_t*)keys)[h];
     if (cur == k) break;
     if (cur == kEmpty) {

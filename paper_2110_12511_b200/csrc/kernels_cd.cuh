@@ -354,6 +354,7 @@ __device__ __forceinline__ void emit(const AggArgs& a, uint32_t u, uint32_t k, u
   // harmless and saves a random load per emitted pair.  With stats on, the
   // decrements that reach live partners are counted separately (bits 36..63 of
   // upd; flush_updates splits them): A_live of the roofline.
+  PBNG_DCHECK(k < a.nU && (MODE == 0 || k != u));
   if (w >= 2 && (MODE == 1 || a.part[k] == kUnassigned)) {
     const uint64_t d = choose2(w);
     if (MODE == 0) {
@@ -579,6 +580,7 @@ __global__ void k_compact(const uint32_t* __restrict__ tv, const uint32_t* __res
       lw += __popc(ml);
       dw += __popc(md);
     }
+    PBNG_DCHECK(lw + dw == L);
     if (ln == 0) {
       ld[v] = lw;
       drop += (unsigned long long)L * L - (unsigned long long)lw * lw;

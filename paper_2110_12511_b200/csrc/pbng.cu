@@ -621,7 +621,7 @@ void reset_tiers(Run& r, State& S) {
 // batches of heavy starts still occupy every SM.  A unit should carry about
 // kMinUnitWedges wedges or more (wedges = the batch's classified wedges).
 #ifndef PBNG_MIN_SPAN
-#define PBNG_MIN_SPAN 16384
+#define PBNG_MIN_SPAN 2048
 #endif
 constexpr uint64_t kMinSpan = PBNG_MIN_SPAN;
 constexpr uint64_t kMinUnitWedges = 1u << 16;
@@ -1228,6 +1228,15 @@ int guarded(Fn&& fn) {
   g_err.clear();
   try {
     fn();
+    if (PBNG_CHECK) {
+      unsigned int line = 0;
+      CK(cudaMemcpyFromSymbol(&line, g_check_line, sizeof(line)));
+      if (line) {
+        const unsigned int zero = 0;
+        CK(cudaMemcpyToSymbol(g_check_line, &zero, sizeof(zero)));
+        fail(PBNG_ERR_CUDA, "device check failed (PBNG_DCHECK) at kernel source line " + std::to_string(line));
+      }
+    }
     return PBNG_OK;
   } catch (const Fail& f) {
     return f.code;
