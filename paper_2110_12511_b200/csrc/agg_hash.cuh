@@ -55,6 +55,10 @@ constexpr uint32_t kHashMaxPb = PBNG_HASH_MAX_PB;       // classify: larger star
 constexpr uint32_t kHW = 32;                            // degree-mass windows
 constexpr uint32_t kRowMin = 64;                        // lists with more entries keep a window-bound row
 constexpr uint32_t kHashChunk = 128;                    // positions per warp step (4 per lane)
+#ifndef PBNG_HASH_BDEPTH
+#define PBNG_HASH_BDEPTH 2
+#endif
+constexpr int kHashBDepth = PBNG_HASH_BDEPTH;           // phase B: 16-byte loads per lane per chunk
 constexpr uint32_t kFiltLog = PBNG_HASH_FILTER_LOG;     // membership filter: 2^kFiltLog bits (16 KB)
 constexpr uint32_t kFiltWords = 1u << (kFiltLog - 5);
 
@@ -402,22 +406,38 @@ __device__ __forceinline__ bool hash_agg_one(const L& lists, uint64_t e0, uint64
     if (gt) {
       const uint32_t hn = S.hlen;
       const uint32_t* hp = partner + S.lbase[hl] + S.seg0[hl];
+      // 16-byte loads: virtual positions q = i + mis over the aligned run ab[],
+      // chunks of 128 * kHashBDepth positions, every lane's kHashBDepth loads
+      // issued before any entry is used (one memory round trip per chunk).  A
+      // load only touches the 16-byte block of a valid entry (never past the
+      // allocation).
+      const uint32_t mis = (uint32_t)(((uintptr_t)hp & 15u) >> 2);
+      const uint4* ab = reinterpret_cast<const uint4*>(hp - mis);
+      const uint32_t qend = hn + mis;
       if (tid == 0) S.next = 0;
       __syncthreads();
       for (;;) {
         uint32_t c = 0;
         if (ln == 0) c = atomicAdd(&S.next, 1u);
-        const uint32_t p0 = __shfl_sync(kFull, c, 0) * kHashChunk;
-        if (p0 >= hn) break;
-        uint32_t x[4];
+        const uint32_t q0 = __shfl_sync(kFull, c, 0) * (128u * kHashBDepth);
+        if (q0 >= qend) break;
+        uint4 v[kHashBDepth];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const uint32_t p = p0 + 32 * j + ln;
-          x[j] = p < hn ? hp[p] : skip;
+        for (int j = 0; j < kHashBDepth; j++) {
+          const uint32_t q = q0 + 128u * j + 4u * ln;
+          v[j] = q < qend ? ab[q >> 2] : make_uint4(skip, skip, skip, skip);
         }
 #pragma unroll
-        for (int j = 0; j < 4; j++)
-          if (x[j] != skip && x[j] < lim && filt_has(S.filt, x[j])) hash_lookup_inc(S.tab, TB, cb, x[j]);
+        for (int j = 0; j < kHashBDepth; j++) {
+          const uint32_t q = q0 + 128u * j + 4u * ln;
+          const uint32_t e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            const uint32_t x = e[t];
+            const bool ok = q + t >= mis && q + t < qend;
+            if (ok && x != skip && x < lim && filt_has(S.filt, x)) hash_lookup_inc(S.tab, TB, cb, x);
+          }
+        }
       }
       __syncthreads();
     }

@@ -763,3 +763,79 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_win(AggArgs a) {
   }
   if (MODE == 1) flush_updates(a, upd);
 }
+
+// List-split mode (CD peel) for small batches of heavy starts over a small live
+// id range: the late CD partitions hold the densest core — a few hundred to a
+// few thousand live vertices, each start with 10^5-10^6 lists of which only a
+// handful of entries are live — where a CTA per start (or per id range) spends
+// its time walking list descriptors one CTA at a time.  Here a unit is (start,
+// list range j of G): the CTA counts w(start, x) over its lists into shared
+// counters over the ids [0, range) (32-bit, one per id; R per-warp copies when
+// the range is small), adds them to the start's global counters gcnt[s][x], and
+// the unit that finishes last (per-start ticket, threadfence pattern) sweeps
+// gcnt[s] and emits C(w,2) for w >= 2.  Every live partner id is
+// below `range` (= 1 + largest live id); stale entries above it are skipped.
+template <int MODE>
+__global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_lsplit(AggArgs a, uint32_t range, uint32_t* gcnt,
+                                                                      uint32_t* done) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  WinSmem& S = *reinterpret_cast<WinSmem*>(wsm);
+  __shared__ WinShared sh;
+  __shared__ uint32_t s_last;
+  const uint32_t tid = threadIdx.x, bd = blockDim.x, wid = tid >> 5, nw = bd >> 5;
+  const uint32_t G = a.win_split;
+  const uint64_t n = (uint64_t)*a.count * G;
+  const auto L = agg_lists<MODE>(a);
+  const uint32_t stride = (range + 3) & ~3u;
+  PBNG_DCHECK(stride <= kWinBitWords);
+  uint32_t R = 1;
+  while (2 * R <= nw && 2 * R * stride <= kWinBitWords) R *= 2;
+  for (uint32_t i = tid; i < R * stride; i += bd) S.bits[i] = 0u;
+  uint32_t* my = S.bits + (wid & (R - 1)) * stride;
+  unsigned long long upd = 0;
+  for (;;) {
+    if (tid == 0) sh.t = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const uint32_t t = sh.t;
+    if (t >= n) break;
+    const uint32_t si = t / G, j = t % G;
+    const uint32_t u = a.list[si].x;
+    const uint64_t e0 = a.offU[u], d = a.offU[u + 1] - e0;
+    const uint64_t l0 = e0 + d * j / G, l1 = e0 + d * (j + 1) / G;
+    // lanes hold entries of up to 32 different (sorted) lists, whose smallest
+    // ids are the same hot core vertices: lanes with equal ids are combined
+    // (match_any) and one lane adds the group's count
+    const uint32_t ln = lane_id();
+    auto f = [&](bool ok, uint32_t x, uint64_t) {
+      const bool act = ok && x != u && x < range;
+      const uint32_t peers = __match_any_sync(kFull, act ? x : 0xFFFFFFFFu);
+      if (act && ln == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&my[x], (uint32_t)__popc(peers));
+    };
+    for (uint64_t c = l0 + 32ull * wid; c < l1; c += 32ull * nw)
+      warp_chunk(L, c, c + 32 < l1 ? c + 32 : l1, a.adjV, 0xFFFFFFFFu, nullptr, nullptr, 0, f);
+    __syncthreads();
+    uint32_t* g = gcnt + (uint64_t)si * stride;
+    for (uint32_t i = tid; i < range; i += bd) {
+      uint32_t v = 0;
+      for (uint32_t r = 0; r < R; r++) {
+        v += S.bits[r * stride + i];
+        S.bits[r * stride + i] = 0u;
+      }
+      if (v) atomicAdd(&g[i], v);
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&done[si], 1u) == G - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      uint64_t acc = 0;
+      for (uint32_t i = tid; i < range; i += bd) {
+        const uint32_t w = __ldcg(&g[i]);
+        if (w >= 2) emit<MODE>(a, u, i, w, acc, upd);
+      }
+    }
+    __syncthreads();
+  }
+  if (MODE == 1) flush_updates(a, upd);
+}

@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256) k_collect_touched(uint32_t nV, uint32_t* 
 // longer ones are chunked over CTAs (k_compact_plan / _count / _scan / _scatter).
 __global__ void k_compact(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ ntv,
                           const uint64_t* __restrict__ offV, uint32_t* adjL, uint32_t* tmp, uint32_t* ld,
-                          const uint32_t* __restrict__ part, uint32_t big, Counters* c) {
+                          const uint32_t* __restrict__ part, uint32_t big, Counters* c, uint32_t thr) {
   const uint32_t ln = lane_id();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -572,7 +572,7 @@ __global__ void k_compact(const uint32_t* __restrict__ tv, const uint32_t* __res
       const uint32_t t = t0 + ln;
       const bool ok = t < L;
       const uint32_t x = ok ? tmp[base + t] : 0u;
-      const bool live = ok && part[x] == kUnassigned;
+      const bool live = ok && part[x] > thr;
       const bool dead = ok && !live;
       const uint32_t ml = __ballot_sync(kFull, live), md = __ballot_sync(kFull, dead);
       if (live) adjL[base + lw + __popc(ml & lanemask_lt())] = x;
@@ -620,7 +620,8 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_count(const uint2* __r
                                                                 const uint32_t* __restrict__ oldL,
                                                                 const uint64_t* __restrict__ offV,
                                                                 const uint32_t* __restrict__ adjL, uint32_t* tmp,
-                                                                const uint32_t* __restrict__ part, uint32_t* cnt) {
+                                                                const uint32_t* __restrict__ part, uint32_t* cnt,
+                                                                uint32_t thr) {
   __shared__ uint32_t s_c;
   const uint32_t nt = *ntask;
   for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_count(const uint2* __r
     for (uint32_t q = a + threadIdx.x; q < b; q += blockDim.x) {
       const uint32_t x = adjL[base + q];
       tmp[base + q] = x;
-      live += part[x] == kUnassigned;
+      live += part[x] > thr;
     }
     live = warp_sum(live);
     if (lane_id() == 0 && live) atomicAdd(&s_c, live);
@@ -674,7 +675,7 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_scatter(const uint2* _
                                                                   const uint64_t* __restrict__ offV,
                                                                   const uint32_t* __restrict__ ld, uint32_t* adjL,
                                                                   const uint32_t* __restrict__ tmp,
-                                                                  const uint32_t* __restrict__ part) {
+                                                                  const uint32_t* __restrict__ part, uint32_t thr) {
   constexpr uint32_t NW = kCompThreads / 32, SL = kCompChunk / NW;  // entries per warp slice
   __shared__ uint32_t s_w[NW];
   const uint32_t w = threadIdx.x >> 5, ln = lane_id();
@@ -688,7 +689,7 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_scatter(const uint2* _
     const uint32_t livepre = cnt[t];
     const uint32_t s0 = a + w * SL, s1 = min(b, s0 + SL);
     uint32_t lw = 0;
-    for (uint32_t q = s0 + ln; q < s1; q += 32) lw += part[tmp[base + q]] == kUnassigned;
+    for (uint32_t q = s0 + ln; q < s1; q += 32) lw += part[tmp[base + q]] > thr;
     lw = warp_sum(lw);
     if (ln == 0) s_w[w] = lw;
     __syncthreads();
@@ -699,7 +700,7 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_scatter(const uint2* _
       const uint32_t q = q0 + ln;
       const bool ok = q < s1;
       const uint32_t x = ok ? tmp[base + q] : 0u;
-      const bool live = ok && part[x] == kUnassigned;
+      const bool live = ok && part[x] > thr;
       const bool dead = ok && !live;
       const uint32_t ml = __ballot_sync(kFull, live), md = __ballot_sync(kFull, dead);
       if (live) adjL[base + lbefore + __popc(ml & lanemask_lt())] = x;

@@ -95,6 +95,7 @@ cudaMemPool_t device_setup(int dev) {
     cudaFuncSetAttribute(k_agg_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
     cudaFuncSetAttribute(k_agg_mid<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem());
     cudaFuncSetAttribute(k_agg_win<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+    cudaFuncSetAttribute(k_agg_lsplit<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
     cudaFuncSetAttribute(k_vp_agg_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_tier_smem());
@@ -464,6 +465,10 @@ struct State {
   uint32_t* rows = nullptr;
   uint32_t cb = 0, dlim = 0;  // count-field bits of a packed slot; starts need fewer lists than dlim
   bool stats = false;         // count live-partner decrements (PBNG_OPT_STATS / _DEFER)
+  // list-split mode of tier 2 (k_agg_lsplit): per-start global counters + finish tickets
+  uint32_t* ls_cnt = nullptr;
+  uint32_t* ls_done = nullptr;
+  uint32_t ls_range = 0;      // > 0: the next PEEL launch uses list-split units over ids [0, ls_range)
 };
 
 uint32_t choose_slots(const Run& r, uint32_t nU) {
@@ -604,7 +609,13 @@ void launch_agg(Run& r, State& S, const uint32_t* ntier) {
     k_agg_hash<MODE><<<r.nsm * kHashCtas, kHashThreads, hash_smem(), r.st>>>(agg_args(S, 1));
     r.post(PBNG_K_AGG_HASH);
   }
-  if (ntier[2] || ntier[1]) {  // tier 1 passes on starts with a window above its capacity
+  if (MODE == 1 && S.ls_range) {
+    r.pre(PBNG_K_AGG_CTA);
+    k_agg_lsplit<1><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2), S.ls_range, S.ls_cnt,
+                                                                        S.ls_done);
+    r.post(PBNG_K_AGG_CTA);
+    S.ls_range = 0;
+  } else if (ntier[2] || ntier[1]) {  // tier 1 passes on starts with a window above its capacity
     r.pre(PBNG_K_AGG_CTA);
     k_agg_win<MODE><<<r.nsm * kWinCtas, kWinThreads, win_smem(), r.st>>>(agg_args(S, 2));
     r.post(PBNG_K_AGG_CTA);
@@ -620,6 +631,9 @@ void reset_tiers(Run& r, State& S) {
 // split wants) when a batch has fewer than two starts per SM, so that small
 // batches of heavy starts still occupy every SM.  A unit should carry about
 // kMinUnitWedges wedges or more (wedges = the batch's classified wedges).
+#ifndef PBNG_LSPLIT
+#define PBNG_LSPLIT 1
+#endif
 #ifndef PBNG_MIN_SPAN
 #define PBNG_MIN_SPAN 2048
 #endif
@@ -632,6 +646,35 @@ uint32_t pick_split(const Run& r, uint32_t n2, uint32_t idspace, uint64_t wedges
   const uint64_t by_work = std::max<uint64_t>(1, wedges / n2 / kMinUnitWedges);
   return (uint32_t)std::max<uint64_t>(1, std::min({want, by_ids, by_work}));
 }
+
+// List-split mode (k_agg_lsplit) for a small tier-2 batch over a small live id range.
+constexpr uint64_t kLsCap = 1ull << 24;  // global counters (64 MB)
+#ifndef PBNG_LS_MAX_IDS
+#define PBNG_LS_MAX_IDS 8192
+#endif
+// live id ranges up to this use list-split units (measured on config 5: at 12K-28K live
+// ids the windowed kernel split by id range is faster; at a few thousand and below,
+// list-split units are)
+constexpr uint32_t kLsMaxIds = PBNG_LS_MAX_IDS < kWinBitWords ? PBNG_LS_MAX_IDS : kWinBitWords;
+void plan_lsplit(Run& r, State& S, const Counters& hc) {
+  S.ls_range = 0;
+  const uint64_t n2 = (uint64_t)hc.ntier[2] + hc.ntier[1];  // tier 1 may pass starts on
+  const uint64_t stride = ((uint64_t)S.idspace + 3) & ~3ull;
+  if (hc.ntier[2] == 0 || hc.ntier[2] >= 2u * (uint32_t)r.nsm * kWinCtas || S.idspace > kLsMaxIds ||
+      n2 * stride > kLsCap)
+    return;
+  if (!S.ls_cnt) {
+    S.ls_cnt = r.alloc<uint32_t>(kLsCap);
+    S.ls_done = r.alloc<uint32_t>(kLsCap / 4);
+  }
+  CK(cudaMemsetAsync(S.ls_cnt, 0, n2 * stride * 4, r.st));
+  CK(cudaMemsetAsync(S.ls_done, 0, n2 * 4, r.st));
+  S.ls_range = S.idspace;
+  const uint64_t want = (2ull * (uint64_t)r.nsm * kWinCtas + hc.ntier[2] - 1) / hc.ntier[2];
+  const uint64_t by_work = std::max<uint64_t>(1, hc.wedges / hc.ntier[2] / kMinUnitWedges);
+  S.win_split = (uint32_t)std::max<uint64_t>(1, std::min(want, by_work));
+}
+
 
 // Vertex-priority count (Alg.1, kernels_vp.cuh) of every unassigned u on the
 // live graph: starts in U, then starts in V; supports accumulate atomically.
@@ -705,7 +748,8 @@ void count_live(Run& r, State& S) {
   launch_agg<0>(r, S, hc.ntier);
 }
 
-void compact(Run& r, State& S, uint32_t epoch, bool force = false) {
+// live entries: part[x] > thr (default: not yet peeled; PBNG- replay: partitions above thr)
+void compact(Run& r, State& S, uint32_t epoch, bool force = false, uint32_t thr = kUnassigned - 1) {
   (void)epoch;
   const uint32_t big = kCompChunk;
   CK(cudaMemsetAsync(&S.c->ntouched, 0, 4, r.st));
@@ -715,7 +759,7 @@ void compact(Run& r, State& S, uint32_t epoch, bool force = false) {
   r.post(PBNG_K_COMPACT);
   r.pre(PBNG_K_COMPACT);
   k_compact<<<r.nsm * 8, 256, 0, r.st>>>(S.touched, &S.c->ntouched, S.g.offV, S.adjL, S.tmp, S.ld, S.part, big,
-                                         S.c);
+                                         S.c, thr);
   r.post(PBNG_K_COMPACT);
   // lists of >= big entries: chunked over CTAs
   r.pre(PBNG_K_COMPACT);
@@ -724,7 +768,7 @@ void compact(Run& r, State& S, uint32_t epoch, bool force = false) {
   r.post(PBNG_K_COMPACT);
   r.pre(PBNG_K_COMPACT);
   k_compact_count<<<r.nsm * 4, kCompThreads, 0, r.st>>>(S.comp_task, S.comp_ntask, S.touched, S.comp_oldL, S.g.offV,
-                                                        S.adjL, S.tmp, S.part, S.comp_cnt);
+                                                        S.adjL, S.tmp, S.part, S.comp_cnt, thr);
   r.post(PBNG_K_COMPACT);
   r.pre(PBNG_K_COMPACT);
   k_compact_scan<<<r.nsm, 256, 0, r.st>>>(S.touched, &S.c->ntouched, big, S.comp_tbase, S.comp_oldL, S.comp_cnt,
@@ -733,7 +777,7 @@ void compact(Run& r, State& S, uint32_t epoch, bool force = false) {
   r.pre(PBNG_K_COMPACT);
   k_compact_scatter<<<r.nsm * 4, kCompThreads, 0, r.st>>>(S.comp_task, S.comp_ntask, S.touched, S.comp_oldL,
                                                           S.comp_tbase, S.comp_cnt, S.g.offV, S.ld, S.adjL, S.tmp,
-                                                          S.part);
+                                                          S.part, thr);
   r.post(PBNG_K_COMPACT);
   // window-bound rows of the compacted lists (tier 1)
   r.pre(PBNG_K_COMPACT);
@@ -855,6 +899,7 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         st.recounts++;
       } else {
         S.win_split = pick_split(r, hc.ntier[2], S.idspace, hc.wedges);
+        if (PBNG_LSPLIT) plan_lsplit(r, S, hc);
         launch_agg<1>(r, S, hc.ntier);
         if (trace) tm = r.event();
         if (del) compact(r, S, epoch);
@@ -865,10 +910,21 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
         rows.push_back(row);
       }
     }
-    compact(r, S, epoch, true);  // partition end: every list grouped by partition for FD
+    if (del) compact(r, S, epoch, true);  // partition end: every list grouped by partition for FD
     scale = part_wc ? (double)first_wc / (double)part_wc : 1.0;
   }
   plan.nparts = (uint32_t)plan.bounds.size() - 1;
+  if (!del) {
+    // PBNG- (no dynamic graph updates): the lists kept every peeled
+    // entry during CD; FD's induced-subgraph layout (each N_v grouped by
+    // partition, latest first) is built once now, by replaying the partition-end
+    // compaction per partition: step p moves the entries of partition p behind
+    // the entries of later partitions.
+    for (uint32_t p = 0; p < plan.nparts; p++) {
+      CK(cudaMemsetAsync(S.vflag, 1, (size_t)S.g.nV * 4, r.st));
+      compact(r, S, epoch, true, p);
+    }
+  }
   if (plan.nparts) plan.bounds.back() = kInf;
   if (trace) {
     const Counters hc = r.readback(S.c);

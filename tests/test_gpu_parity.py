@@ -293,6 +293,21 @@ def _config3_theta(g):
     return _C3["theta"]
 
 
+def test_config3_ablations(pb):
+    """PBNG- (no dynamic graph updates: peeled entries stay in every list through CD, the
+    FD layout is built after CD) and PBNG-- (also no batch re-count), on
+    config 3: θ equals the oracle's, and without deletion CD traverses more wedges
+    (deletion is what saves them)."""
+    g, P = gg.config(3)
+    d = dev(pb, g)
+    want = _config3_theta(g)
+    _, st0 = pb.pbng_tip_decompose(d, P, opts=pb.OPT_STATS)
+    for opts in (pb.OPT_NO_DELETE, pb.OPT_NO_DELETE | pb.OPT_NO_RECOUNT):
+        tip, st = pb.pbng_tip_decompose(d, P, opts=opts | pb.OPT_STATS)
+        assert np.array_equal(pb.as_u64(tip), want), opts
+        assert st["wedges_cd"] > st0["wedges_cd"], (opts, st["wedges_cd"], st0["wedges_cd"])
+
+
 @pytest.mark.parametrize("P", [1, 3, 8])
 def test_fd_grid_path_tiny(pb, P):
     """FD on the whole GPU (host-driven rounds), forced for every small partition."""
