@@ -802,14 +802,8 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_lsplit(AggArgs a,
     const uint32_t u = a.list[si].x;
     const uint64_t e0 = a.offU[u], d = a.offU[u + 1] - e0;
     const uint64_t l0 = e0 + d * j / G, l1 = e0 + d * (j + 1) / G;
-    // lanes hold entries of up to 32 different (sorted) lists, whose smallest
-    // ids are the same hot core vertices: lanes with equal ids are combined
-    // (match_any) and one lane adds the group's count
-    const uint32_t ln = lane_id();
     auto f = [&](bool ok, uint32_t x, uint64_t) {
-      const bool act = ok && x != u && x < range;
-      const uint32_t peers = __match_any_sync(kFull, act ? x : 0xFFFFFFFFu);
-      if (act && ln == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&my[x], (uint32_t)__popc(peers));
+      if (ok && x != u && x < range) atomicAdd(&my[x], 1u);
     };
     for (uint64_t c = l0 + 32ull * wid; c < l1; c += 32ull * nw)
       warp_chunk(L, c, c + 32 < l1 ? c + 32 : l1, a.adjV, 0xFFFFFFFFu, nullptr, nullptr, 0, f);
