@@ -29,24 +29,24 @@
 // (included inside namespace pbng by kernels_cd.cuh, after agg_win.cuh)
 
 #ifndef PBNG_HASH_SLOTS
-#define PBNG_HASH_SLOTS 19456
+#define PBNG_HASH_SLOTS 10240
 #endif
 #ifndef PBNG_HASH_FILTER_LOG
-#define PBNG_HASH_FILTER_LOG 17
+#define PBNG_HASH_FILTER_LOG 16
 #endif
 #ifndef PBNG_HASH_FILTER
 #define PBNG_HASH_FILTER 1
 #endif
 #ifndef PBNG_HASH_THREADS
-#define PBNG_HASH_THREADS 512
+#define PBNG_HASH_THREADS 384
 #endif
 #ifndef PBNG_HASH_CTAS
-#define PBNG_HASH_CTAS 2
+#define PBNG_HASH_CTAS 3
 #endif
 #ifndef PBNG_HASH_MAX_PB
 #define PBNG_HASH_MAX_PB (1u << 17)
 #endif
-constexpr uint32_t kHashSlots = PBNG_HASH_SLOTS;        // 76 KB table per CTA
+constexpr uint32_t kHashSlots = PBNG_HASH_SLOTS;        // 40 KB table per CTA, 3 CTAs per SM
 constexpr uint32_t kHashThreads = PBNG_HASH_THREADS;
 constexpr uint32_t kHashCtas = PBNG_HASH_CTAS;          // resident CTAs per SM
 constexpr uint32_t kHashCap = kHashSlots / 2;           // entries per group (distinct partners <= entries): load <= 1/2
@@ -59,7 +59,7 @@ constexpr uint32_t kHashChunk = 128;                    // positions per warp st
 #define PBNG_HASH_BDEPTH 2
 #endif
 constexpr int kHashBDepth = PBNG_HASH_BDEPTH;           // phase B: 16-byte loads per lane per chunk
-constexpr uint32_t kFiltLog = PBNG_HASH_FILTER_LOG;     // membership filter: 2^kFiltLog bits (16 KB)
+constexpr uint32_t kFiltLog = PBNG_HASH_FILTER_LOG;     // membership filter: 2^kFiltLog bits (8 KB)
 constexpr uint32_t kFiltWords = 1u << (kFiltLog - 5);
 
 struct HashSmem {

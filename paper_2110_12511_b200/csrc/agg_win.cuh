@@ -60,9 +60,6 @@ constexpr int kDenseDepth = PBNG_DENSE_DEPTH;
 #ifndef PBNG_COMBINE
 #define PBNG_COMBINE 0
 #endif
-#ifndef PBNG_WIN_PREFETCH
-#define PBNG_WIN_PREFETCH 1
-#endif
 #ifndef PBNG_COMBINE_DENSE
 #define PBNG_COMBINE_DENSE 0
 #endif
@@ -195,48 +192,6 @@ __device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64
     fn(ok, ok ? p[t + ln] : 0u);
   }
 }
-
-// A chunk's entries p[i0, i1) (at most 128 * D) held in registers: load() issues
-// every load of the chunk at once (unaligned head, D aligned 16-byte loads per
-// lane, tail), visit() later runs fn(ok, x) over them warp-convergently, in the
-// same order as seg_visit.  Lets a warp fetch its first chunk of the next
-// window before the window barrier (round 2: the tier-2 kernel was
-// barrier-bound, each window waiting on its slowest warp's first load).
-template <int D>
-struct ChunkRegs {
-  uint4 v[D];
-  uint32_t hx, tx;
-  uint64_t i0, h, t, i1;
-  __device__ __forceinline__ void load(const uint32_t* __restrict__ p, uint64_t a0, uint64_t a1) {
-    const uint32_t ln = lane_id();
-    i0 = a0;
-    i1 = a1;
-    h = (i0 + 3) & ~3ull;
-    if (h > i1) h = i1;
-    t = h + ((i1 - h) & ~3ull);
-    hx = i0 + ln < h ? p[i0 + ln] : 0u;
-#pragma unroll
-    for (int j = 0; j < D; j++) {
-      const uint64_t q = h + 128 * j + 4 * ln;
-      v[j] = q < t ? __ldg(reinterpret_cast<const uint4*>(p + q)) : make_uint4(0, 0, 0, 0);
-    }
-    tx = t + ln < i1 ? p[t + ln] : 0u;
-  }
-  template <class Fn>
-  __device__ __forceinline__ void visit(Fn& fn) const {
-    const uint32_t ln = lane_id();
-    fn(i0 + ln < h, hx);
-#pragma unroll
-    for (int j = 0; j < D; j++) {
-      const bool ok = h + 128 * j + 4 * ln < t;
-      fn(ok, v[j].x);
-      fn(ok, v[j].y);
-      fn(ok, v[j].z);
-      fn(ok, v[j].w);
-    }
-    fn(t + ln < i1, tx);
-  }
-};
 
 // Mark the entries p[i0, i1) (all inside the window starting at `a`) in the
 // bitmap; repeats go to the table.
@@ -545,16 +500,6 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
   }
   __syncthreads();
   if (prof && tid == 0) atomicAdd(&prof_clk[1], (unsigned long long)(clock64() - tp0));
-  // first chunk of this warp in the next fast-path window, loaded before the
-  // window barrier (starts with <= 32 lists: the chunk -> list map of a window
-  // is one ballot over its prefix row)
-  ChunkRegs<kSegDepth> pf;
-  uint32_t pf_k = 0xFFFFFFFFu;
-  const bool use_pf = !Pass2::kOn && pre && PBNG_WIN_FAST && PBNG_WIN_PREFETCH && nl <= 32;
-  auto fast_win = [&](uint32_t kk) {
-    const uint32_t r = kk - k0;
-    return S.ek[r] != 0 && S.ek[r] <= kDenseEntries && bitmap_chunk(S.ek[r]) == kWinChunk;
-  };
   for (uint32_t k = k0; k < k1; k++) {
     const uint64_t wa = lo + (uint64_t)k * kWinIds;
     const uint64_t wb = wa + kWinIds < hi ? wa + kWinIds : hi;
@@ -595,59 +540,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       };
       const long long tm0 = clock64();
       // kSegDepth 16-byte loads per lane in flight per warp step (chunk = 128 * kSegDepth entries: one step)
-      if (use_pf) {
-        // chunk wid is this warp's (prefetched when pf_k == k); the rest are taken dynamically
-        auto one = [&](bool ok, uint32_t x) {
-          const bool act = ok && x != skip;
-          const uint32_t o = x - (uint32_t)wa;
-          PBNG_DCHECK(!act || o < kWinIds);
-          const uint32_t bit = 1u << (o & 31);
-          if (act && (atomicOr(&S.bits[o >> 5], bit) & bit)) win_dup_insert(S, sh, x);
-        };
-        auto chunk_of = [&](uint32_t c, uint64_t& q0, uint64_t& q1) {
-          uint32_t lo = 0, hi = (uint32_t)nl;
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (crow[mid] <= c) lo = mid; else hi = mid;
-          }
-          const uint64_t sbeg = gbase[lo] + bnd[(uint64_t)lo * W1 + k], send = gbase[lo] + bnd[(uint64_t)lo * W1 + k + 1];
-          q0 = sbeg + (uint64_t)(c - crow[lo]) * wch;
-          q1 = q0 + wch < send ? q0 + wch : send;
-        };
-        if (wid < tot) {
-          if (pf_k != k) {
-            uint64_t q0, q1;
-            chunk_of(wid, q0, q1);
-            pf.load(partner, q0, q1);
-          }
-          pf.visit(one);
-        }
-        for (;;) {
-          uint32_t c = 0;
-          if (ln == 0) c = atomicAdd(&sh.next, 1u);
-          c = __shfl_sync(kFull, c, 0) + nw;
-          if (c >= tot) break;
-          uint64_t q0, q1;
-          chunk_of(c, q0, q1);
-          ChunkRegs<kSegDepth> cr;
-          cr.load(partner, q0, q1);
-          cr.visit(one);
-        }
-        // fetch this warp's first chunk of the next fast-path window
-        pf_k = 0xFFFFFFFFu;
-        const uint32_t k2 = k + 1;
-        if (k2 < k1 && fast_win(k2) && wid < S.ctot[k2 - k0]) {
-          const uint32_t* cp2 = cpg + (uint64_t)(k2 - k0) * PL;
-          const uint32_t cv = ln < nl ? cp2[ln] : 0xFFFFFFFFu;
-          const uint32_t li = (uint32_t)__popc(__ballot_sync(kFull, cv <= wid)) - 1u;
-          const uint32_t cl = __shfl_sync(kFull, cv, li);
-          const uint64_t sbeg = gbase[li] + bnd[(uint64_t)li * W1 + k2];
-          const uint64_t send = gbase[li] + bnd[(uint64_t)li * W1 + k2 + 1];
-          const uint64_t q0 = sbeg + (uint64_t)(wid - cl) * kWinChunk;
-          pf.load(partner, q0, q0 + kWinChunk < send ? q0 + kWinChunk : send);
-          pf_k = k2;
-        }
-      } else if (wch > kWinChunk)
+      if (wch > kWinChunk)
         run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<2 * kSegDepth>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
       else
         run([&](uint64_t i0, uint64_t i1, uint64_t) { win_mark<kSegDepth>(partner, i0, i1, (uint32_t)wa, skip, S, sh); });
@@ -912,8 +805,10 @@ __global__ void __launch_bounds__(kWinThreads, kWinCtas) k_agg_lsplit(AggArgs a,
     auto f = [&](bool ok, uint32_t x, uint64_t) {
       if (ok && x != u && x < range) atomicAdd(&my[x], 1u);
     };
-    for (uint64_t c = l0 + 32ull * wid; c < l1; c += 32ull * nw)
-      warp_chunk(L, c, c + 32 < l1 ? c + 32 : l1, a.adjV, 0xFFFFFFFFu, nullptr, nullptr, 0, f);
+    // lists in chunks of blockDim (a warp per 32 lists, short lists flattened
+    // over the lanes); lists of >= blockDim entries are walked by the whole CTA
+    // (in the dense core a start's few thousand lists each hold most live ids)
+    cta_wedges(L, l0, l1, a.adjV, S.segS, &sh.ndup, f);
     __syncthreads();
     uint32_t* g = gcnt + (uint64_t)si * stride;
     for (uint32_t i = tid; i < range; i += bd) {
