@@ -8,6 +8,8 @@ the paper.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
   count(g)            -> uint64 support per u    (oracle.c: oracle_count)
   count_subset(g, us) -> uint64 support per listed u
   bup_tip(g)          -> uint64 tip number per u (oracle.c: oracle_bup_tip)
+  edge_count(g)       -> uint64 butterflies per edge, U-side CSR order
+                         (oracle.c: oracle_edge_count, P:353-354, P:427-430)
   tip_level(g, θ, k)  -> (uint32 k-tip label per u, number of k-tips)
                          (oracle.c: oracle_tip_level, P:451-475)
   brute.*             pure-Python brute force and Definition-2 tip numbers for
@@ -15,7 +17,9 @@ the paper.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 
 Parity status: count and bup_tip are pinned by tests/test_oracle.py (brute-force
 4-tuple enumeration, K_{a,b} closed form, Σ_U = Σ_V identity, Definition-2 tip
-numbers, golden graphs).  No function here is "parity unpinned".
+numbers, golden graphs); edge_count by 4-tuple enumeration, the K_{a,b} closed
+form (a-1)(b-1), the transposed-graph traversal edge by edge, Σ_e = 4·#butterflies,
+Σ_{e∋u} = 2·⋈_u and hand-derived goldens (tests/golden/edge_counts.txt).  No function here is "parity unpinned".
 """
 from __future__ import annotations
 
@@ -60,7 +64,8 @@ def _load():
         _lib.oracle_count_subset.argtypes = base + [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                                     ctypes.POINTER(Stats)]
         _lib.oracle_bup_tip.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
-        for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip):
+        _lib.oracle_edge_count.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
+        for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip, _lib.oracle_edge_count):
             f.restype = ctypes.c_int
         _lib.oracle_tip_level.argtypes = base + [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
         _lib.oracle_tip_level.restype = ctypes.c_int64
@@ -104,6 +109,19 @@ def count_subset(g, us, stats: Stats | None = None) -> np.ndarray:
     if _load().oracle_count_subset(g.nU, g.nV, *ptrs, us.ctypes.data, us.shape[0], out.ctypes.data,
                                    ctypes.byref(st)):
         raise MemoryError("oracle_count_subset failed")
+    del keep
+    return out
+
+
+def edge_count(g, stats: Stats | None = None) -> np.ndarray:
+    """Per-edge butterfly count ⋈_e (Alg.1 per-edge output P:398),
+    indexed by the edge's position in the U-side CSR (g.adj_u): the plain definition
+    Σ_{u' ∈ N_v, u' ≠ u} (w(u,u') − 1) for e = (u, v)."""
+    keep, ptrs = _csr(g)
+    out = np.zeros(g.m, np.uint64)
+    st = stats if stats is not None else Stats()
+    if _load().oracle_edge_count(g.nU, g.nV, *ptrs, out.ctypes.data, ctypes.byref(st)):
+        raise MemoryError("oracle_edge_count failed")
     del keep
     return out
 

@@ -108,3 +108,15 @@ def k_tips(g, k):
         label[u] = min(cls[u])
         roots.add(label[u])
     return label, len(roots)
+
+
+def edge_butterflies(g):
+    """Per-edge butterfly counts from the 4-tuples (notation table): each
+    butterfly (u, u', v, v') adds one to each of its four edges.  Returned in the
+    U-side CSR order of g (position of (u, v) in g.adj_u)."""
+    _, _, _, tuples = butterflies(g)
+    c = {}
+    for (u, u2, v, v2) in tuples:
+        for e in ((u, v), (u, v2), (u2, v), (u2, v2)):
+            c[e] = c.get(e, 0) + 1
+    return [c.get((u, int(g.adj_u[e])), 0) for u in range(g.nU) for e in range(int(g.off_u[u]), int(g.off_u[u + 1]))]

@@ -21,6 +21,9 @@
  *                    Alg.2 l.11 P:526 / S:259; tie-break lowest id, reading g2).
  *   oracle_count_subset  oracle_count restricted to a list of u (for sampled
  *                    checks at sizes where the full oracle is too slow).
+ *   oracle_edge_count per-edge butterfly count (notation table P:353-354,
+ *                    Alg.1 per-edge output P:398) by its plain
+ *                    definition: sum over u' in N_v \ {u} of (w(u,u') - 1).
  *   oracle_tip_level one level of the k-tip hierarchy from tip numbers
  *                    (k-tip = Def. 2): members
  *                    U_k = {theta >= k}, V(H) = V; two members are adjacent
@@ -86,6 +89,51 @@ int oracle_count_subset(uint32_t nU, uint32_t nV, const uint64_t* offU, const ui
 int oracle_count(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
                  const uint64_t* offV, const uint32_t* adjV, uint64_t* support, oracle_stats* st) {
   return oracle_count_subset(nU, nV, offU, adjU, offV, adjV, NULL, 0, support, st);
+}
+
+/* Per-edge butterfly count (notation table: "no. of butterflies in G
+ * that contain edge e"; the per-edge output of Alg.1).
+ * The plain definition written out: a butterfly through e = (u, v) is a pair
+ * (u', v') with u' != u, v' != v and edges (u, v'), (u', v), (u', v'); for a
+ * fixed u' in N_v \ {u} the admissible v' are N_u ∩ N_u' \ {v}, of which
+ * there are w(u,u') - 1 (v itself is common).  So
+ *     edge_support[e] = sum_{u' in N_v, u' != u} (w(u,u') - 1),
+ * w from the same dense counters as oracle_count.  edge_support is indexed by
+ * the position e of the edge in the U-side CSR (offU/adjU). */
+int oracle_edge_count(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
+                      const uint64_t* offV, const uint32_t* adjV, uint64_t* edge_support, oracle_stats* st) {
+  (void)nV;
+  uint32_t* cnt = (uint32_t*)calloc(nU ? nU : 1, sizeof(uint32_t));
+  uint32_t* touched = (uint32_t*)malloc((nU ? nU : 1) * sizeof(uint32_t));
+  if (!cnt || !touched) { free(cnt); free(touched); return -1; }
+  uint64_t wedges = 0;
+  for (uint32_t u = 0; u < nU; u++) {
+    uint64_t nt = 0;
+    for (uint64_t e = offU[u]; e < offU[u + 1]; e++) {
+      uint32_t v = adjU[e];
+      for (uint64_t f = offV[v]; f < offV[v + 1]; f++) {
+        uint32_t u2 = adjV[f];
+        wedges++;
+        if (u2 == u) continue;
+        if (cnt[u2]++ == 0) touched[nt++] = u2;
+      }
+    }
+    for (uint64_t e = offU[u]; e < offU[u + 1]; e++) {
+      uint32_t v = adjU[e];
+      uint64_t s = 0;
+      for (uint64_t f = offV[v]; f < offV[v + 1]; f++) {
+        uint32_t u2 = adjV[f];
+        if (u2 == u) continue;
+        s += cnt[u2] - 1;
+      }
+      edge_support[e] = s;
+    }
+    for (uint64_t t = 0; t < nt; t++) cnt[touched[t]] = 0;
+  }
+  if (st) st->wedges += 2 * wedges;
+  free(cnt);
+  free(touched);
+  return 0;
 }
 
 /* ---- indexed binary min-heap keyed by (support, id) --------------------- */

@@ -269,3 +269,71 @@ def test_brute_init_support_pins():
             part = [int(x) for x in rng.integers(0, 3, a)]
             want = [sum(1 for x in range(a) if x != u and part[x] >= part[u]) * comb(b, 2) for u in range(a)]
             assert brute.init_support(g, part) == want
+
+
+# ---- per-edge butterfly counts (Alg.1 per-edge part P:427-430)
+
+def _mirror(g):
+    """mirror[e] = position in g's V-side CSR of the edge at U-side position e."""
+    pos = {}
+    for v in range(g.nV):
+        for f in range(int(g.off_v[v]), int(g.off_v[v + 1])):
+            pos[(int(g.adj_v[f]), v)] = f
+    return np.array([pos[(u, int(g.adj_u[e]))] for u in range(g.nU)
+                     for e in range(int(g.off_u[u]), int(g.off_u[u + 1]))], np.int64)
+
+
+def test_edge_count_golden():
+    for name, sizes, edges, want in _parse(os.path.join(GOLD, "edge_counts.txt")):
+        nu, nv = map(int, sizes.split())
+        el = _edges(edges)
+        g = gg.from_edges(nu, nv, el)
+        got = dict(zip([(u, int(g.adj_u[e])) for u in range(g.nU)
+                        for e in range(int(g.off_u[u]), int(g.off_u[u + 1]))], oracle.edge_count(g)))
+        assert [int(got[e]) for e in el] == [int(x) for x in want.split()], name
+
+
+@pytest.mark.parametrize("a", range(1, 6))
+@pytest.mark.parametrize("b", range(1, 6))
+def test_edge_count_complete_bipartite(a, b):
+    """K_{a,b}: every edge lies in (a-1)(b-1) butterflies."""
+    assert list(oracle.edge_count(gg.complete(a, b))) == [(a - 1) * (b - 1)] * (a * b)
+
+
+def test_edge_count_equals_bruteforce_4tuples():
+    """Each butterfly adds one to each of its four edges (4-tuple enumeration); the
+    count from the V side (oracle on the transposed graph, a different traversal)
+    agrees edge by edge; Σ_e ⋈_e = 4·#butterflies and Σ_{e ∋ u} ⋈_e = 2·⋈_u."""
+    for g in _tiny_corpus(n=200, seed0=9000):
+        ec = oracle.edge_count(g)
+        assert list(ec) == brute.edge_butterflies(g)
+        ecv = oracle.edge_count(g.swapped())
+        assert np.array_equal(ecv[_mirror(g)], ec)
+        _, _, total, _ = brute.butterflies(g)
+        assert int(ec.sum()) == 4 * total
+        per_u = np.zeros(g.nU, np.uint64)
+        for u in range(g.nU):
+            per_u[u] = ec[int(g.off_u[u]):int(g.off_u[u + 1])].sum()
+        assert np.array_equal(per_u, 2 * oracle.count(g))
+
+
+def test_edge_count_config_identities():
+    """Config 1 and 2 (20K / 197K edges): both traversal directions agree edge by edge,
+    and the per-vertex sums are twice the vertex counts on both sides."""
+    for cfg in (1, "2a"):
+        g, _ = gg.config(cfg)
+        ec = oracle.edge_count(g)
+        ecv = oracle.edge_count(g.swapped())
+        assert np.array_equal(ecv[_mirror(g)], ec)
+        du = np.diff(g.off_u).astype(np.int64)
+        per_u = np.where(du > 0, np.add.reduceat(ec, np.minimum(g.off_u[:-1], g.m - 1).astype(np.int64)), 0)
+        assert np.array_equal(per_u, 2 * oracle.count(g))
+        assert int(ec.sum()) == 2 * int(oracle.count(g).sum())
+    # config 2a closed form: block K_{a,b} edges have (a-1)(b-1)
+    g, _ = gg.config("2a")
+    ec = oracle.edge_count(g)
+    du = np.diff(g.off_u).astype(np.int64)
+    dv = np.diff(g.off_v).astype(np.int64)
+    u_of_e = np.repeat(np.arange(g.nU), du)
+    want = (du[u_of_e] - 1) * (dv[g.adj_u.astype(np.int64)] - 1)
+    assert np.array_equal(ec, want.astype(np.uint64))
