@@ -10,6 +10,8 @@ the paper.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
   bup_tip(g)          -> uint64 tip number per u (oracle.c: oracle_bup_tip)
   edge_count(g)       -> uint64 butterflies per edge, U-side CSR order
                          (oracle.c: oracle_edge_count, P:353-354, P:427-430)
+  bup_wing(g)         -> uint64 wing number per edge, U-side CSR order
+                         (oracle.c: oracle_bup_wing, Alg.2)
   tip_level(g, θ, k)  -> (uint32 k-tip label per u, number of k-tips)
                          (oracle.c: oracle_tip_level, P:451-475)
   brute.*             pure-Python brute force and Definition-2 tip numbers for
@@ -65,7 +67,9 @@ def _load():
                                                     ctypes.POINTER(Stats)]
         _lib.oracle_bup_tip.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
         _lib.oracle_edge_count.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
-        for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip, _lib.oracle_edge_count):
+        _lib.oracle_bup_wing.argtypes = base + [ctypes.c_void_p, ctypes.POINTER(Stats)]
+        for f in (_lib.oracle_count, _lib.oracle_count_subset, _lib.oracle_bup_tip, _lib.oracle_edge_count,
+                  _lib.oracle_bup_wing):
             f.restype = ctypes.c_int
         _lib.oracle_tip_level.argtypes = base + [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
         _lib.oracle_tip_level.restype = ctypes.c_int64
@@ -122,6 +126,18 @@ def edge_count(g, stats: Stats | None = None) -> np.ndarray:
     st = stats if stats is not None else Stats()
     if _load().oracle_edge_count(g.nU, g.nV, *ptrs, out.ctypes.data, ctypes.byref(st)):
         raise MemoryError("oracle_edge_count failed")
+    del keep
+    return out
+
+
+def bup_wing(g, stats: Stats | None = None) -> np.ndarray:
+    """Wing number of every edge (U-side CSR order) by sequential bottom-up edge
+    peeling, Alg.2 as written (P:508-531)."""
+    keep, ptrs = _csr(g)
+    out = np.zeros(g.m, np.uint64)
+    st = stats if stats is not None else Stats()
+    if _load().oracle_bup_wing(g.nU, g.nV, *ptrs, out.ctypes.data, ctypes.byref(st)):
+        raise MemoryError("oracle_bup_wing failed")
     del keep
     return out
 

@@ -120,3 +120,35 @@ def edge_butterflies(g):
         for e in ((u, v), (u, v2), (u2, v), (u2, v2)):
             c[e] = c.get(e, 0) + 1
     return [c.get((u, int(g.adj_u[e])), 0) for u in range(g.nU) for e in range(int(g.off_u[u]), int(g.off_u[u + 1]))]
+
+
+def wing_by_definition(g):
+    """Wing number of every edge by Definition 1 and the wing-number
+    definition: θ_e = the largest k such that e survives the iterated
+    removal of edges in fewer than k butterflies of the remaining subgraph (the
+    maximal subgraph in which every edge has >= k butterflies; connectivity splits
+    it into k-wings but does not change which edges it holds).  From the 4-tuples,
+    U-side CSR order."""
+    _, _, _, tuples = butterflies(g)
+    edges = [(u, int(g.adj_u[e])) for u in range(g.nU) for e in range(int(g.off_u[u]), int(g.off_u[u + 1]))]
+    bfs = [((u, v), (u, v2), (u2, v), (u2, v2)) for (u, u2, v, v2) in tuples]
+    theta = {e: 0 for e in edges}
+    k = 1
+    while True:
+        live = set(edges)
+        while True:
+            cnt = {e: 0 for e in live}
+            for b in bfs:
+                if all(x in live for x in b):
+                    for x in b:
+                        cnt[x] += 1
+            drop = {e for e in live if cnt[e] < k}
+            if not drop:
+                break
+            live -= drop
+        if not live:
+            break
+        for e in live:
+            theta[e] = k
+        k += 1
+    return [theta[e] for e in edges]

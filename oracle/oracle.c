@@ -24,6 +24,9 @@
  *   oracle_edge_count per-edge butterfly count (notation table P:353-354,
  *                    Alg.1 per-edge output P:398) by its plain
  *                    definition: sum over u' in N_v \ {u} of (w(u,u') - 1).
+ *   oracle_bup_wing  wing decomposition by sequential bottom-up peeling of
+ *                    edges, Alg.2 as written, wing numbers per
+ *                    U-CSR position.
  *   oracle_tip_level one level of the k-tip hierarchy from tip numbers
  *                    (k-tip = Def. 2): members
  *                    U_k = {theta >= k}, V(H) = V; two members are adjacent
@@ -244,6 +247,88 @@ int oracle_bup_tip(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_
   }
   if (st) { st->wedges += local.wedges; st->updates += local.updates; st->peeled += local.peeled; }
   free(support); free(alive); free(cnt); free(touched); free(h.heap); free(h.pos);
+  return 0;
+}
+
+/* ---- wing decomposition (edges) ------------------------------------------
+ * Bottom-up peeling of edges exactly as Alg.2: support = per-edge
+ * butterfly counts (l.1, oracle_edge_count), repeatedly peel the edge of
+ * minimum support (l.3, tie-break lowest U-CSR position), theta_e = its support
+ * (l.4), and for every butterfly (u,v,u',v') of the current graph through
+ * e = (u,v) (l.7-10: v' in N_u \ {v}, u' in N_v' \ {u} with (u',v) in E(G))
+ * set support <- max(theta_e, support - 1) on e1=(u,v'), e2=(u',v), e3=(u',v')
+ * (l.11).  theta is indexed by U-CSR position.  Edge lookup by binary search
+ * in sorted copies of the U lists. */
+typedef struct { uint32_t v; uint32_t e; } vpos;
+static int vpos_cmp(const void* a, const void* b) {
+  uint32_t x = ((const vpos*)a)->v, y = ((const vpos*)b)->v;
+  return x < y ? -1 : (x > y);
+}
+static int64_t find_edge(const uint64_t* offU, const vpos* sorted, uint32_t u, uint32_t v) {
+  uint64_t lo = offU[u], hi = offU[u + 1];
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) / 2;
+    if (sorted[mid].v < v) lo = mid + 1; else hi = mid;
+  }
+  return (lo < offU[u + 1] && sorted[lo].v == v) ? (int64_t)sorted[lo].e : -1;
+}
+
+int oracle_bup_wing(uint32_t nU, uint32_t nV, const uint64_t* offU, const uint32_t* adjU,
+                    const uint64_t* offV, const uint32_t* adjV, uint64_t* theta, oracle_stats* st) {
+  uint64_t m = offU[nU];
+  if (m == 0) return 0;
+  if (m >= UINT32_MAX) return -1;
+  uint64_t* support = (uint64_t*)malloc(m * sizeof(uint64_t));
+  unsigned char* alive = (unsigned char*)malloc(m);
+  uint32_t* row = (uint32_t*)malloc(m * sizeof(uint32_t));
+  vpos* sorted = (vpos*)malloc(m * sizeof(vpos));
+  iheap h;
+  h.heap = (uint32_t*)malloc(m * sizeof(uint32_t));
+  h.pos = (uint32_t*)malloc(m * sizeof(uint32_t));
+  if (!support || !alive || !row || !sorted || !h.heap || !h.pos) return -1;
+  oracle_stats local = {0, 0, 0};
+  if (oracle_edge_count(nU, nV, offU, adjU, offV, adjV, support, &local)) return -1;
+  for (uint32_t u = 0; u < nU; u++) {
+    for (uint64_t e = offU[u]; e < offU[u + 1]; e++) {
+      row[e] = u;
+      sorted[e].v = adjU[e];
+      sorted[e].e = (uint32_t)e;
+    }
+    qsort(sorted + offU[u], offU[u + 1] - offU[u], sizeof(vpos), vpos_cmp);
+  }
+  h.key = support;
+  h.size = (uint32_t)m;
+  for (uint32_t e = 0; e < m; e++) { h.heap[e] = e; h.pos[e] = e; alive[e] = 1; }
+  for (int64_t i = (int64_t)m / 2 - 1; i >= 0; i--) down_(&h, (uint32_t)i);
+  while (h.size) {
+    uint32_t e = pop_(&h);
+    uint64_t th = support[e];
+    theta[e] = th;
+    alive[e] = 0;
+    local.peeled++;
+    uint32_t u = row[e], v = adjU[e];
+    for (uint64_t e1 = offU[u]; e1 < offU[u + 1]; e1++) {
+      if (!alive[e1]) continue;           /* e1 = (u, v') in E(G), v' != v (e is gone) */
+      uint32_t v2 = adjU[e1];
+      for (uint64_t f = offV[v2]; f < offV[v2 + 1]; f++) {
+        uint32_t u2 = adjV[f];
+        local.wedges++;
+        if (u2 == u) continue;
+        int64_t e3 = find_edge(offU, sorted, u2, v2);   /* (u', v') */
+        int64_t e2 = find_edge(offU, sorted, u2, v);    /* (u', v)  */
+        if (e3 < 0 || e2 < 0 || !alive[e3] || !alive[e2]) continue;
+        uint64_t ids[3] = {e1, (uint64_t)e2, (uint64_t)e3};
+        for (int j = 0; j < 3; j++) {
+          uint64_t x = ids[j], s = support[x];
+          uint64_t ns = s > th ? s - 1 : th;  /* max(theta_e, s - 1) */
+          local.updates++;
+          if (ns != s) { support[x] = ns; up_(&h, h.pos[x]); }
+        }
+      }
+    }
+  }
+  if (st) { st->wedges += local.wedges; st->updates += local.updates; st->peeled += local.peeled; }
+  free(support); free(alive); free(row); free(sorted); free(h.heap); free(h.pos);
   return 0;
 }
 

@@ -337,3 +337,44 @@ def test_edge_count_config_identities():
     u_of_e = np.repeat(np.arange(g.nU), du)
     want = (du[u_of_e] - 1) * (dv[g.adj_u.astype(np.int64)] - 1)
     assert np.array_equal(ec, want.astype(np.uint64))
+
+
+# ---- wing decomposition (Alg.2)
+
+def test_wing_golden():
+    for name, sizes, edges, want in _parse(os.path.join(GOLD, "wing_numbers.txt")):
+        nu, nv = map(int, sizes.split())
+        el = _edges(edges)
+        g = gg.from_edges(nu, nv, el)
+        got = dict(zip([(u, int(g.adj_u[e])) for u in range(g.nU)
+                        for e in range(int(g.off_u[u]), int(g.off_u[u + 1]))], oracle.bup_wing(g)))
+        assert [int(got[e]) for e in el] == [int(x) for x in want.split()], name
+        assert brute.wing_by_definition(g) == [int(got[(u, v)]) for u in range(g.nU)
+                                               for v in g.adj_u[int(g.off_u[u]):int(g.off_u[u + 1])]], name
+
+
+@pytest.mark.parametrize("a", range(1, 6))
+@pytest.mark.parametrize("b", range(1, 6))
+def test_wing_complete_bipartite(a, b):
+    """K_{a,b} is one ((a-1)(b-1))-wing."""
+    assert list(oracle.bup_wing(gg.complete(a, b))) == [(a - 1) * (b - 1)] * (a * b)
+
+
+def test_wing_equals_definition():
+    """Alg.2 BUP = Definition 1 (iterated removal over the 4-tuples) on 150 tiny graphs;
+    the transposed graph gives the same wing number per edge; θ_e <= ⋈_e."""
+    for g in _tiny_corpus(n=150, seed0=12000):
+        th = oracle.bup_wing(g)
+        assert list(th) == brute.wing_by_definition(g)
+        assert np.array_equal(oracle.bup_wing(g.swapped())[_mirror(g)], th)
+        assert np.all(th <= oracle.edge_count(g))
+
+
+def test_wing_config2a_blocks():
+    """Config 2a (200 disjoint K_{a,b}): θ_e = (a-1)(b-1) of the edge's block."""
+    g, _ = gg.config("2a")
+    du = np.diff(g.off_u).astype(np.int64)
+    dv = np.diff(g.off_v).astype(np.int64)
+    u_of_e = np.repeat(np.arange(g.nU), du)
+    want = (du[u_of_e] - 1) * (dv[g.adj_u.astype(np.int64)] - 1)
+    assert np.array_equal(oracle.bup_wing(g), want.astype(np.uint64))
