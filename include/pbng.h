@@ -99,6 +99,7 @@ enum {
   PBNG_K_FD_BUILD = 8,  /* partition membership, segments, LPT work */
   PBNG_K_FD = 9,        /* k_fd: persistent fine-grained peeling */
   PBNG_K_COUNT_VP = 10, /* vertex-priority counting kernels (when used) */
+  PBNG_K_EDGE = 11,     /* per-edge butterfly counting (k_edge_*) */
   PBNG_K_NUM = 16
 };
 
@@ -130,6 +131,65 @@ enum {
  * P:393-426) on the degree-relabeled graph.  out_support: device, peel-side
  * n entries. */
 int pbng_count_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_support, void* stream);
+
+/* Per-edge butterfly counts (⋈_e = number of butterflies of G that contain
+ * edge e, notation table) by vertex-priority counting, the per-edge
+ * part of Alg.1 (pveBcnt; l.27-30: every wedge (mid, last) of a
+ * start whose endpoint pair closes c >= 2 wedges adds c - 1 to its two edges).
+ *   side               0: out_edge_support[i] is the count of the edge at
+ *                      position i of U.indices (row = the U vertex whose
+ *                      offsets range holds i); 1: same in V's CSR order.
+ *   out_edge_support   device, m entries (uint64).
+ *   out_info           HOST array of 4 or NULL: [0] Alg.1 wedges expanded (each
+ *                      (start, mid, last) with last ranked above mid and start,
+ *                      starts on both sides); [1..3] starts routed to the warp /
+ *                      CTA-hash / dense tiers (kernels_edge.cuh).
+ * The graph must be simple (no repeated (u, v)); lists need not be sorted.
+ * Errors: PBNG_ERR_ARG (null pointers, U.m != V.m), PBNG_ERR_OOM, PBNG_ERR_CUDA.
+ * Synchronous: returns after the result is written. */
+int pbng_count_edge_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_edge_support,
+                                uint64_t* out_info, void* stream);
+
+/* BE-Index (Bloom-Edge-Index), built from the
+ * wedges of vertex-priority counting as P:627-634 describes: every pair
+ * {start, last} of same-side vertices with c >= 2 common Alg.1 wedges (last
+ * ranked above start and above the mids) is the dominant set of a maximal
+ * priority bloom with bloom number k_B = c (Definition); its twin
+ * edge pairs are ({start, mid}, {mid, last}) for every such mid.
+ * Two-call protocol: with bloom_off == NULL only out_sizes is written; then
+ * call again with caller-allocated DEVICE arrays of those sizes:
+ *   out_sizes   HOST uint64[2]: number of blooms nb, number of twin pairs np
+ *   bloom_off   uint64[nb+1]: pairs of bloom b are [bloom_off[b], bloom_off[b+1])
+ *   bloom_k     uint32[nb]: bloom number k_B (= bloom_off[b+1] - bloom_off[b])
+ *   bloom_dom   uint32[2*nb]: dominant set (x, y) in caller labels, x = the
+ *               start, y = last (highest priority); bit 31 of x set when the
+ *               dominant set lies in V
+ *   pairs       uint32[2*np]: twin pair (e1, e2) as positions in U.indices
+ *               (e1 = {start, mid}, e2 = {mid, last})
+ * The bloom set depends on the priority order among equal degrees (any
+ * order is a valid BE-Index); every butterfly lies in exactly one bloom
+ * (Property) and every edge in k_B - 1 butterflies of each bloom
+ * holding it (Property).  Errors: PBNG_ERR_ARG, PBNG_ERR_OOM
+ * (also when np >= 2^32), PBNG_ERR_CUDA.  Synchronous. */
+int pbng_be_index(pbng_csr U, pbng_csr V, uint64_t* out_sizes, uint64_t* bloom_off, uint32_t* bloom_k,
+                  uint32_t* bloom_dom, uint32_t* pairs, void* stream);
+
+/* Wing decomposition (wing number θ_e, Definition P:441-449;
+ * SURVEY §8(f) f4): BE-Index construction, then level-synchronous peeling of
+ * all edges with support <= the current level, with the batch bloom update
+ * (a bloom B losing d of its k_B twin pairs in a round takes k_B - 1 from
+ * each surviving twin of a lost pair and d from each edge of a kept pair,
+ * the update of Alg.3 P:644-674 applied to a batch as P:1452-1490).
+ * Exact (the result equals bottom-up peeling, Alg.2).
+ *   side        0: out_theta in U.indices order; 1: in V.indices order.
+ *   out_theta   device uint64[m].
+ *   out_info    HOST uint64[4] or NULL: blooms, twin pairs, level scans,
+ *               peeling rounds.
+ * Memory: the BE-Index takes about 37 B per twin pair (at most the Alg.1
+ * wedges of pbng_count_edge_butterflies); PBNG_ERR_OOM when it does not fit.
+ * The paper's CD/FD partitioning of wing decomposition is not
+ * used: every level is one global batch.  Errors as above.  Synchronous. */
+int pbng_wing_decompose(pbng_csr U, pbng_csr V, int side, uint64_t* out_theta, uint64_t* out_info, void* stream);
 
 /* Tip decomposition of the peel side (tip number θ_u):
  *   count (Alg.1) -> coarse-grained decomposition CD into <= P ranges

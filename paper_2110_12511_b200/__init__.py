@@ -32,7 +32,7 @@ OPT_FD_GRID, OPT_STATS_DEFER = 64, 128
 MAX_P = 4096
 KERNEL_FAMILIES = ("init", "classify", "agg_warp", "agg_cta", "agg_hash", "select", "range", "compact",
                    "fd_build", "fd", "count_vp")
-EXPORTS = ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
+EXPORTS = ("pbng_count_butterflies", "pbng_count_edge_butterflies", "pbng_be_index", "pbng_wing_decompose", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
            "pbng_tip_components", "pbng_kernel_times", "pbng_release_memory", "pbng_last_error", "pbng_version")
 
 
@@ -78,6 +78,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
         lib = ctypes.CDLL(path)
         lib.pbng_count_butterflies.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        lib.pbng_count_edge_butterflies.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                                    ctypes.c_void_p]
+        lib.pbng_be_index.argtypes = [Csr, Csr] + [ctypes.c_void_p] * 6
+        lib.pbng_wing_decompose.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         lib.pbng_tip_decompose.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p,
                                            ctypes.c_uint32, ctypes.POINTER(Stats), ctypes.c_void_p]
         lib.pbng_tip_decompose_host.argtypes = lib.pbng_tip_decompose.argtypes
@@ -86,7 +90,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pbng_tip_components.argtypes = [Csr, Csr, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         for f in ("pbng_count_butterflies", "pbng_tip_decompose", "pbng_tip_decompose_host", "pbng_tip_plan",
-                  "pbng_tip_components"):
+                  "pbng_tip_components", "pbng_count_edge_butterflies", "pbng_be_index", "pbng_wing_decompose"):
             getattr(lib, f).restype = ctypes.c_int
         lib.pbng_kernel_times.argtypes = [ctypes.c_void_p]
         lib.pbng_kernel_times.restype = ctypes.c_int
@@ -163,6 +167,55 @@ def pbng_count_butterflies(g: DeviceGraph, side: int = 0, out=None, stream=None)
     _check(load_library().pbng_count_butterflies(U, V, side, ctypes.c_void_p(out.data_ptr() if n else None),
                                                  _stream_ptr(stream)))
     return out
+
+
+def pbng_count_edge_butterflies(g: DeviceGraph, side: int = 0, out=None, stream=None):
+    """Per-edge butterfly counts in the CSR order of `side` (0: g.adj_u positions, 1: g.adj_v);
+    returns (int64 tensor of uint64 bits, info dict: Alg.1 wedges expanded, starts per tier)."""
+    torch = _torch()
+    m = int(g.m)
+    if out is None:
+        out = torch.empty(m, dtype=torch.int64, device=g.off_u.device)
+    info = (ctypes.c_uint64 * 4)()
+    U, V = g.csrs()
+    _check(load_library().pbng_count_edge_butterflies(U, V, side, ctypes.c_void_p(out.data_ptr() if m else None),
+                                                      info, _stream_ptr(stream)))
+    return out, {"wedges": int(info[0]), "tiers": [int(x) for x in info[1:]]}
+
+
+def pbng_be_index(g: DeviceGraph, stream=None):
+    """BE-Index: dict of numpy arrays bloom_off (uint64), bloom_k (uint32), dom (uint32 [nb,2],
+    bit 31 of dom[:,0] = dominant set in V), pairs (uint32 [np,2], positions in g.adj_u)."""
+    torch = _torch()
+    sizes = (ctypes.c_uint64 * 2)()
+    U, V = g.csrs()
+    lib = load_library()
+    _check(lib.pbng_be_index(U, V, sizes, None, None, None, None, _stream_ptr(stream)))
+    nb, np_ = int(sizes[0]), int(sizes[1])
+    dv = g.off_u.device
+    off = torch.empty(nb + 1, dtype=torch.int64, device=dv)
+    k = torch.empty(max(nb, 1), dtype=torch.int32, device=dv)
+    dom = torch.empty(max(2 * nb, 1), dtype=torch.int32, device=dv)
+    pairs = torch.empty(max(2 * np_, 1), dtype=torch.int32, device=dv)
+    _check(lib.pbng_be_index(U, V, sizes, ctypes.c_void_p(off.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+                             ctypes.c_void_p(dom.data_ptr()), ctypes.c_void_p(pairs.data_ptr()), _stream_ptr(stream)))
+    assert int(sizes[0]) == nb and int(sizes[1]) == np_
+    u32 = lambda t, n: t[:n].cpu().numpy().view(np.uint32)  # noqa: E731
+    return {"bloom_off": off.cpu().numpy().view(np.uint64), "bloom_k": u32(k, nb),
+            "dom": u32(dom, 2 * nb).reshape(nb, 2), "pairs": u32(pairs, 2 * np_).reshape(np_, 2)}
+
+
+def pbng_wing_decompose(g: DeviceGraph, side: int = 0, out=None, stream=None):
+    """Wing numbers per edge in the CSR order of `side`; returns (int64 tensor of uint64 bits, info)."""
+    torch = _torch()
+    m = int(g.m)
+    if out is None:
+        out = torch.empty(m, dtype=torch.int64, device=g.off_u.device)
+    info = (ctypes.c_uint64 * 4)()
+    U, V = g.csrs()
+    _check(load_library().pbng_wing_decompose(U, V, side, ctypes.c_void_p(out.data_ptr() if m else None), info,
+                                              _stream_ptr(stream)))
+    return out, {"blooms": int(info[0]), "pairs": int(info[1]), "levels": int(info[2]), "rounds": int(info[3])}
 
 
 def pbng_tip_decompose(g: DeviceGraph, P: int, side: int = 0, opts: int = 0, out=None, stream=None):
@@ -250,3 +303,6 @@ tip_decompose = pbng_tip_decompose
 tip_plan = pbng_tip_plan
 tip_decompose_host = pbng_tip_decompose_host
 tip_components = pbng_tip_components
+count_edge_butterflies = pbng_count_edge_butterflies
+be_index = pbng_be_index
+wing_decompose = pbng_wing_decompose

@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "../../include/pbng.h"
+#include "kernels_edge.cuh"
+#include "kernels_wing.cuh"
 #include "kernels_fd.cuh"
 #include "kernels_level.cuh"
 #include "kernels_relabel.cuh"
@@ -55,6 +57,11 @@ size_t mid_smem() { return sizeof(MidSmem); }
 size_t win_smem() { return sizeof(WinSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
 size_t hash_smem() { return sizeof(HashSmem); }
+size_t edge_warp_smem() { return (size_t)(kEdgeWarpThreads / 32) * (2 * (1u << kEdgeWarpLog) + kEdgeWarpPb) * 4; }
+size_t edge_cta_smem() { return ((size_t)2 * (1u << kEdgeCtaLog) + kEdgeCtaPb) * 4; }
+size_t edge_dense_smem() {
+  return std::max<size_t>((size_t)kEdgeDenseSmem, (size_t)2 * (1u << kEdgeBigLog) + kEdgeBigCap) * 4;
+}
 size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kFdCtaSlots + kFdThreads) * 4; }
 
 // Per-device one-time setup: the dynamic shared-memory opt-ins (they apply to
@@ -107,6 +114,9 @@ cudaMemPool_t device_setup(int dev) {
     CK(cudaFuncSetAttribute(k_agg_hash<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
     CK(cudaFuncSetAttribute(k_agg_hash<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
     CK(cudaFuncSetAttribute(k_vp_agg_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hash_smem()));
+    CK(cudaFuncSetAttribute(k_edge_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_warp_smem()));
+    CK(cudaFuncSetAttribute(k_edge_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_cta_smem()));
+    CK(cudaFuncSetAttribute(k_edge_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_dense_smem()));
     CK(cudaGetLastError());
   }
   g_dev_ready[dev] = true;
@@ -1279,6 +1289,362 @@ uint32_t tip_level(const Dev& g, const uint64_t* tip, uint64_t k, uint32_t* out_
   return n;
 }
 
+// Per-edge butterfly counts (Alg.1 per-edge part, kernels_edge.cuh): starts in
+// U, then starts in V, each routed into three tiers; then every caller edge
+// gathers accU[p] + accV[q] from its two relabeled positions.  g is oriented
+// so that U is the output side.
+void edge_count(const Dev& g, uint64_t* out, uint64_t* out_info, cudaStream_t s) {
+  uint64_t info[4] = {0, 0, 0, 0};
+  Run r(s);
+  SideRank RU, RV;
+  const Dev gr = relabel(r, g, RU, RV);
+  uint32_t* cutU = r.alloc<uint32_t>(g.nU);
+  uint32_t* cutV = r.alloc<uint32_t>(g.nV);
+  uint32_t* ld = r.alloc<uint32_t>(g.nV);
+  unsigned long long* cnt = r.alloc<unsigned long long>(2);  // [0] Σ d², [1] wedges
+  CK(cudaMemsetAsync(cnt, 0, 16, r.st));
+  r.pre(PBNG_K_EDGE);
+  k_vp_cut_u<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, gr.offU, gr.adjU, RV.binoff, RV.dmax, cutU);
+  r.post(PBNG_K_EDGE);
+  if (g.nV) {
+    r.pre(PBNG_K_EDGE);
+    k_init_v<<<r.nsm * 4, 256, 0, r.st>>>(g.nV, gr.offV, ld, cnt);
+    r.post(PBNG_K_EDGE);
+    r.pre(PBNG_K_EDGE);
+    k_vp_cut_v<<<r.nsm * 8, 256, 0, r.st>>>(g.nV, gr.offV, gr.adjV, ld, RU.binoff, RU.dmax, cutV);
+    r.post(PBNG_K_EDGE);
+  }
+  uint64_t* accU = r.alloc<uint64_t>(g.m);
+  uint64_t* accV = r.alloc<uint64_t>(g.m);
+  CK(cudaMemsetAsync(accU, 0, g.m * 8, r.st));
+  CK(cudaMemsetAsync(accV, 0, g.m * 8, r.st));
+  const uint32_t nmax = std::max(g.nU, g.nV);
+  uint2* q = r.alloc<uint2>(3ull * nmax);
+  uint32_t* nq = r.alloc<uint32_t>(4);
+  uint32_t* dense = nullptr;
+  uint32_t ndense = 0;
+  for (int side = 0; side < 2; side++) {
+    EdgeArgs a;
+    a.nS = side == 0 ? g.nU : g.nV;
+    a.offS = side == 0 ? gr.offU : gr.offV;
+    a.adjS = side == 0 ? gr.adjU : gr.adjV;
+    a.offM = side == 0 ? gr.offV : gr.offU;
+    a.adjM = side == 0 ? gr.adjV : gr.adjU;
+    a.cutM = side == 0 ? cutV : cutU;
+    a.accS = side == 0 ? accU : accV;
+    a.accM = side == 0 ? accV : accU;
+    a.q = q;
+    a.nq = nq;
+    a.wedges = cnt + 1;
+    a.dense = nullptr;
+    if (a.nS == 0) continue;
+    CK(cudaMemsetAsync(nq, 0, 16, r.st));
+    r.pre(PBNG_K_EDGE);
+    k_edge_classify<<<r.nsm * 8, 256, 0, r.st>>>(a);
+    r.post(PBNG_K_EDGE);
+    uint32_t hq[4];
+    CK(cudaMemcpyAsync(hq, nq, 16, cudaMemcpyDeviceToHost, r.st));
+    CK(cudaStreamSynchronize(r.st));
+    for (int t = 0; t < 3; t++) info[1 + t] += hq[t];
+    if (hq[0]) {
+      r.pre(PBNG_K_EDGE);
+      k_edge_warp<<<std::min<uint32_t>(r.nsm * 3, (hq[0] + 7) / 8), kEdgeWarpThreads, edge_warp_smem(), r.st>>>(a);
+      r.post(PBNG_K_EDGE);
+    }
+    if (hq[1]) {
+      r.pre(PBNG_K_EDGE);
+      k_edge_cta<<<std::min<uint32_t>(r.nsm * 2, hq[1]), kEdgeCtaThreads, edge_cta_smem(), r.st>>>(a);
+      r.post(PBNG_K_EDGE);
+    }
+    if (hq[2]) {
+      const uint32_t want = std::min<uint32_t>(r.nsm, hq[2]);
+      if (a.nS > kEdgeDenseSmem && ndense < want) {  // per-CTA dense counters for start ids above the smem range
+        size_t freeb = 0, totalb = 0;
+        CK(cudaMemGetInfo(&freeb, &totalb));
+        const uint64_t per = (uint64_t)nmax * 4;
+        ndense = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (freeb / 2) / per));
+        dense = r.alloc<uint32_t>((uint64_t)ndense * nmax);
+        CK(cudaMemsetAsync(dense, 0, (uint64_t)ndense * per, r.st));
+      }
+      a.dense = dense;
+      const uint32_t grid = a.nS > kEdgeDenseSmem ? std::min(want, ndense) : want;
+      r.pre(PBNG_K_EDGE);
+      k_edge_dense<<<grid, kEdgeDenseThreads, edge_dense_smem(), r.st>>>(a);
+      r.post(PBNG_K_EDGE);
+    }
+  }
+  if (g.m) {
+    r.pre(PBNG_K_EDGE);
+    k_edge_gather<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.m, g.offU, g.adjU, RU.rank, RV.rank, gr.offU, gr.adjU,
+                                                 gr.offV, gr.adjV, accU, accV, out);
+    r.post(PBNG_K_EDGE);
+  }
+  info[0] = read_u64(r, cnt + 1);
+  if (out_info) std::memcpy(out_info, info, sizeof(info));
+}
+
+// ------------------------------------------------------------ BE-Index / wing
+struct BeIndex {
+  uint64_t nb = 0, np = 0;
+  unsigned long long* bloom_off = nullptr;
+  uint32_t* bloom_k = nullptr;
+  uint2* bloom_dom = nullptr;
+  uint2* pair = nullptr;
+  uint32_t* pair_bloom = nullptr;
+};
+
+// BE-Index of the relabeled graph gr (kernels_wing.cuh): sizes run over the
+// starts of both sides, one exclusive scan over [U starts | V starts], fill run.
+void be_build(Run& r, const Dev& gr, const SideRank& RU, const SideRank& RV, BeIndex& I) {
+  if (gr.nU >= 0x80000000u || gr.nV >= 0x80000000u) fail(PBNG_ERR_ARG, "BE-Index needs fewer than 2^31 vertices per side");
+  uint32_t* cutU = r.alloc<uint32_t>(gr.nU);
+  uint32_t* cutV = r.alloc<uint32_t>(gr.nV);
+  uint32_t* ld = r.alloc<uint32_t>(gr.nV);
+  unsigned long long* sq = r.alloc<unsigned long long>(1);
+  CK(cudaMemsetAsync(sq, 0, 8, r.st));
+  r.pre(PBNG_K_EDGE);
+  k_vp_cut_u<<<r.nsm * 8, 256, 0, r.st>>>(gr.nU, gr.offU, gr.adjU, RV.binoff, RV.dmax, cutU);
+  r.post(PBNG_K_EDGE);
+  r.pre(PBNG_K_EDGE);
+  k_init_v<<<r.nsm * 4, 256, 0, r.st>>>(gr.nV, gr.offV, ld, sq);
+  r.post(PBNG_K_EDGE);
+  r.pre(PBNG_K_EDGE);
+  k_vp_cut_v<<<r.nsm * 8, 256, 0, r.st>>>(gr.nV, gr.offV, gr.adjV, ld, RU.binoff, RU.dmax, cutV);
+  r.post(PBNG_K_EDGE);
+  uint32_t* mir = r.alloc<uint32_t>(gr.m);
+  r.pre(PBNG_K_EDGE);
+  k_be_mirror<<<r.nsm * 8, 256, 0, r.st>>>(gr.nV, gr.m, gr.offV, gr.adjV, gr.offU, gr.adjU, mir);
+  r.post(PBNG_K_EDGE);
+  const uint32_t nmax = std::max(gr.nU, gr.nV);
+  size_t freeb = 0, totalb = 0;
+  CK(cudaMemGetInfo(&freeb, &totalb));
+  const uint32_t ctas = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>({(uint64_t)r.nsm * 4, (uint64_t)nmax, (freeb / 4) / (12ull * nmax)}));
+  uint32_t* cnt = r.alloc<uint32_t>((uint64_t)ctas * nmax);
+  uint32_t* bidx = r.alloc<uint32_t>((uint64_t)ctas * nmax);
+  uint32_t* pbase = r.alloc<uint32_t>((uint64_t)ctas * nmax);
+  CK(cudaMemsetAsync(cnt, 0, (uint64_t)ctas * nmax * 4, r.st));
+  CK(cudaMemsetAsync(bidx, 0xFF, (uint64_t)ctas * nmax * 4, r.st));
+  const uint64_t nsz = (uint64_t)gr.nU + 1 + gr.nV + 1;
+  unsigned long long* nbs = r.alloc<unsigned long long>(nsz);
+  unsigned long long* nps = r.alloc<unsigned long long>(nsz);
+  CK(cudaMemsetAsync(nbs, 0, nsz * 8, r.st));
+  CK(cudaMemsetAsync(nps, 0, nsz * 8, r.st));
+  uint32_t* ticket = r.alloc<uint32_t>(1);
+  auto args = [&](int side) {
+    BeArgs b;
+    std::memset(&b, 0, sizeof(b));
+    EdgeArgs& a = b.a;
+    a.nS = side == 0 ? gr.nU : gr.nV;
+    a.offS = side == 0 ? gr.offU : gr.offV;
+    a.adjS = side == 0 ? gr.adjU : gr.adjV;
+    a.offM = side == 0 ? gr.offV : gr.offU;
+    a.adjM = side == 0 ? gr.adjV : gr.adjU;
+    a.cutM = side == 0 ? cutV : cutU;
+    b.mirM2U = mir;
+    b.mirS2U = mir;
+    b.side = (uint32_t)side;
+    b.cnt = cnt;
+    b.bidx = bidx;
+    b.pbase = pbase;
+    const uint64_t o = side == 0 ? 0 : (uint64_t)gr.nU + 1;
+    b.nb_s = nbs + o;
+    b.np_s = nps + o;
+    b.bS = nbs + o;
+    b.pS = nps + o;
+    b.ticket = ticket;
+    return b;
+  };
+  for (int side = 0; side < 2; side++) {
+    BeArgs b = args(side);
+    if (!b.a.nS) continue;
+    CK(cudaMemsetAsync(ticket, 0, 4, r.st));
+    r.pre(PBNG_K_EDGE);
+    k_be_build<false><<<std::min<uint32_t>(ctas, b.a.nS), kBeThreads, 0, r.st>>>(b);
+    r.post(PBNG_K_EDGE);
+  }
+  scan_u64(r, nbs, nsz);
+  scan_u64(r, nps, nsz);
+  // totals: the scan's last entry is the sum of everything before it (its own input is 0)
+  I.nb = read_u64(r, nbs + nsz - 1);
+  I.np = read_u64(r, nps + nsz - 1);
+  if (I.np >= 0xFFFFFFFFull) fail(PBNG_ERR_OOM, "BE-Index has 2^32 or more twin pairs");
+  I.bloom_off = r.alloc<unsigned long long>(I.nb + 1);
+  I.bloom_k = r.alloc<uint32_t>(I.nb);
+  I.bloom_dom = r.alloc<uint2>(I.nb);
+  I.pair = r.alloc<uint2>(I.np);
+  I.pair_bloom = r.alloc<uint32_t>(I.np);
+  CK(cudaMemcpyAsync(I.bloom_off + I.nb, &I.np, 8, cudaMemcpyHostToDevice, r.st));
+  for (int side = 0; side < 2; side++) {
+    BeArgs b = args(side);
+    if (!b.a.nS) continue;
+    b.bloom_off = I.bloom_off;
+    b.bloom_k = I.bloom_k;
+    b.bloom_dom = I.bloom_dom;
+    b.pair = I.pair;
+    b.pair_bloom = I.pair_bloom;
+    CK(cudaMemsetAsync(ticket, 0, 4, r.st));
+    r.pre(PBNG_K_EDGE);
+    k_be_build<true><<<std::min<uint32_t>(ctas, b.a.nS), kBeThreads, 0, r.st>>>(b);
+    r.post(PBNG_K_EDGE);
+  }
+  CK(cudaStreamSynchronize(r.st));  // &I.np must outlive its copy
+}
+
+// Wing decomposition of gr on its BE-Index (kernels_wing.cuh): θ per canonical edge id.
+void wing_peel(Run& r, const Dev& gr, const BeIndex& I, uint64_t* theta, uint64_t* info) {
+  const uint64_t m = gr.m;
+  WingArgs w;
+  std::memset(&w, 0, sizeof(w));
+  w.m = m;
+  w.nb = I.nb;
+  w.bloom_off = I.bloom_off;
+  w.bloom_k = I.bloom_k;
+  w.pair = I.pair;
+  w.pair_bloom = I.pair_bloom;
+  w.theta = theta;
+  w.bloom_d = r.alloc<uint32_t>(I.nb);
+  CK(cudaMemsetAsync(w.bloom_d, 0, I.nb * 4, r.st));
+  w.pstate = r.alloc<uint32_t>(I.np);
+  CK(cudaMemsetAsync(w.pstate, 0, I.np * 4, r.st));
+  w.sup = r.alloc<unsigned long long>(m);
+  CK(cudaMemsetAsync(w.sup, 0, m * 8, r.st));
+  unsigned long long* ioff = r.alloc<unsigned long long>(m + 1);
+  unsigned long long* cur = r.alloc<unsigned long long>(m + 1);
+  CK(cudaMemsetAsync(ioff, 0, (m + 1) * 8, r.st));
+  uint32_t* inc = r.alloc<uint32_t>(2 * I.np);
+  if (I.np) {
+    r.pre(PBNG_K_FD);
+    k_wing_init<<<r.nsm * 8, 256, 0, r.st>>>(w);
+    r.post(PBNG_K_FD);
+    r.pre(PBNG_K_FD);
+    k_wing_inc_count<<<r.nsm * 8, 256, 0, r.st>>>(w, ioff);
+    r.post(PBNG_K_FD);
+  }
+  scan_u64(r, ioff, m + 1);
+  CK(cudaMemcpyAsync(cur, ioff, (m + 1) * 8, cudaMemcpyDeviceToDevice, r.st));
+  if (I.np) {
+    r.pre(PBNG_K_FD);
+    k_wing_inc_fill<<<r.nsm * 8, 256, 0, r.st>>>(w, cur, inc);
+    r.post(PBNG_K_FD);
+  }
+  w.inc_off = ioff;
+  w.inc = inc;
+  w.alive = r.alloc<uint8_t>(m);
+  CK(cudaMemsetAsync(w.alive, 1, m, r.st));
+  uint32_t* live[2] = {r.alloc<uint32_t>(m), r.alloc<uint32_t>(m)};
+  r.pre(PBNG_K_FD);
+  k_iota<<<r.nsm * 8, 256, 0, r.st>>>(m, live[0]);
+  r.post(PBNG_K_FD);
+  uint32_t* SX[2] = {r.alloc<uint32_t>(m), r.alloc<uint32_t>(m)};
+  w.T = r.alloc<uint32_t>(std::max<uint64_t>(I.nb, 1));
+  w.ctl = r.alloc<WingCtl>(1);
+  WingCtl* hctl = nullptr;
+  CK(cudaMallocHost(&hctl, sizeof(WingCtl)));
+  struct HostFree {
+    WingCtl* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{hctl};
+  uint64_t k = 0, levels = 0, rounds = 0;
+  uint32_t nlive = (uint32_t)m, cur_live = 0;
+  const WingCtl zero{0, 0, 0, 0, ~0ull};
+  for (;;) {
+    // level scan: compact the live list, minimum live support
+    CK(cudaMemcpyAsync(w.ctl, &zero, sizeof(WingCtl), cudaMemcpyHostToDevice, r.st));
+    w.live = live[cur_live];
+    r.pre(PBNG_K_FD);
+    k_wing_scan<<<std::max<uint32_t>(1, std::min<uint32_t>(r.nsm * 8, (nlive + 255) / 256)), 256, 0, r.st>>>(
+        w, nlive, live[cur_live], live[cur_live ^ 1]);
+    r.post(PBNG_K_FD);
+    CK(cudaMemcpyAsync(hctl, w.ctl, sizeof(WingCtl), cudaMemcpyDeviceToHost, r.st));
+    CK(cudaStreamSynchronize(r.st));
+    cur_live ^= 1;
+    nlive = hctl->nlive;
+    if (nlive == 0) break;
+    k = std::max<uint64_t>(k, hctl->minsup);
+    levels++;
+    w.live = live[cur_live];
+    w.S = SX[0];
+    CK(cudaMemsetAsync(&w.ctl->nS, 0, 4, r.st));
+    r.pre(PBNG_K_FD);
+    k_wing_select<<<std::min<uint32_t>(r.nsm * 8, (nlive + 255) / 256), 256, 0, r.st>>>(w, nlive, k);
+    r.post(PBNG_K_FD);
+    CK(cudaMemcpyAsync(hctl, w.ctl, sizeof(WingCtl), cudaMemcpyDeviceToHost, r.st));
+    CK(cudaStreamSynchronize(r.st));
+    uint32_t nS = hctl->nS;
+    int cs = 0;
+    while (nS) {
+      rounds++;
+      w.S = SX[cs];
+      w.X = SX[cs ^ 1];
+      CK(cudaMemsetAsync(&w.ctl->nX, 0, 8, r.st));  // nX, nT
+      r.pre(PBNG_K_FD);
+      k_wing_claim<<<std::min<uint32_t>(r.nsm * 8, (nS + 7) / 8), 256, 0, r.st>>>(w, nS, k);
+      r.post(PBNG_K_FD);
+      r.pre(PBNG_K_FD);
+      k_wing_kill<<<std::min<uint32_t>(r.nsm * 8, (nS + 255) / 256), 256, 0, r.st>>>(w, nS);
+      r.post(PBNG_K_FD);
+      CK(cudaMemcpyAsync(hctl, w.ctl, sizeof(WingCtl), cudaMemcpyDeviceToHost, r.st));
+      CK(cudaStreamSynchronize(r.st));
+      const uint32_t nT = hctl->nT;
+      if (nT) {
+        r.pre(PBNG_K_FD);
+        k_wing_update<<<std::min<uint32_t>(r.nsm * 8, (nT + 7) / 8), 256, 0, r.st>>>(w, nT, k);
+        r.post(PBNG_K_FD);
+      }
+      CK(cudaMemcpyAsync(hctl, w.ctl, sizeof(WingCtl), cudaMemcpyDeviceToHost, r.st));
+      CK(cudaStreamSynchronize(r.st));
+      nS = hctl->nX;
+      cs ^= 1;
+    }
+  }
+  if (info) {
+    info[0] = I.nb;
+    info[1] = I.np;
+    info[2] = levels;
+    info[3] = rounds;
+  }
+}
+
+void wing_decompose(const Dev& g, uint64_t* out, uint64_t* info, cudaStream_t s) {
+  Run r(s);
+  SideRank RU, RV;
+  const Dev gr = relabel(r, g, RU, RV);
+  BeIndex I;
+  be_build(r, gr, RU, RV, I);
+  uint64_t* theta = r.alloc<uint64_t>(g.m);
+  wing_peel(r, gr, I, theta, info);
+  r.pre(PBNG_K_INIT);
+  k_wing_gather<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.m, g.offU, g.adjU, RU.rank, RV.rank, gr.offU, gr.adjU, theta,
+                                              out);
+  r.post(PBNG_K_INIT);
+  CK(cudaStreamSynchronize(r.st));
+}
+
+void be_index_export(const Dev& g, uint64_t* sizes, unsigned long long* bloom_off, uint32_t* bloom_k,
+                     uint32_t* dom, uint32_t* pairs, cudaStream_t s) {
+  Run r(s);
+  SideRank RU, RV;
+  const Dev gr = relabel(r, g, RU, RV);
+  BeIndex I;
+  be_build(r, gr, RU, RV, I);
+  sizes[0] = I.nb;
+  sizes[1] = I.np;
+  if (!bloom_off) return;  // size query
+  uint32_t* r2c = r.alloc<uint32_t>(g.m);
+  r.pre(PBNG_K_INIT);
+  k_edge_r2c<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.m, g.offU, g.adjU, RU.rank, RV.rank, gr.offU, gr.adjU, r2c);
+  r.post(PBNG_K_INIT);
+  CK(cudaMemcpyAsync(bloom_off, I.bloom_off, (I.nb + 1) * 8, cudaMemcpyDeviceToDevice, r.st));
+  if (I.nb) CK(cudaMemcpyAsync(bloom_k, I.bloom_k, I.nb * 4, cudaMemcpyDeviceToDevice, r.st));
+  if (I.nb || I.np) {
+    r.pre(PBNG_K_INIT);
+    k_be_export<<<r.nsm * 8, 256, 0, r.st>>>(I.nb, I.np, I.pair, r2c, I.bloom_dom, RU.inv, RV.inv, pairs, dom);
+    r.post(PBNG_K_INIT);
+  }
+  CK(cudaStreamSynchronize(r.st));
+}
+
 template <class Fn>
 int guarded(Fn&& fn) {
   g_err.clear();
@@ -1325,6 +1691,46 @@ int pbng_count_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_suppo
     k_gather<uint64_t><<<r.nsm * 4, 256, 0, r.st>>>(g.nU, RU.rank, S.support, out_support);
     r.post(PBNG_K_INIT);
     CK(cudaStreamSynchronize(r.st));
+  });
+}
+
+int pbng_count_edge_butterflies(pbng_csr U, pbng_csr V, int side, uint64_t* out_edge_support,
+                                uint64_t* out_info, void* stream) {
+  return guarded([&] {
+    Dev g;
+    orient(U, V, side, g);
+    if (out_info) std::memset(out_info, 0, 4 * sizeof(uint64_t));
+    if (!out_edge_support && g.m) fail(PBNG_ERR_ARG, "out_edge_support is null");
+    if (g.m == 0) return;
+    edge_count(g, out_edge_support, out_info, (cudaStream_t)stream);
+  });
+}
+
+int pbng_be_index(pbng_csr U, pbng_csr V, uint64_t* out_sizes, uint64_t* bloom_off, uint32_t* bloom_k,
+                  uint32_t* bloom_dom, uint32_t* pairs, void* stream) {
+  return guarded([&] {
+    Dev g;
+    orient(U, V, 0, g);
+    if (!out_sizes) fail(PBNG_ERR_ARG, "out_sizes is null");
+    out_sizes[0] = out_sizes[1] = 0;
+    if (bloom_off && !(bloom_k && bloom_dom && pairs)) fail(PBNG_ERR_ARG, "null BE-Index output");
+    if (g.m == 0) {
+      if (bloom_off) CK(cudaMemsetAsync(bloom_off, 0, 8, (cudaStream_t)stream));
+      CK(cudaStreamSynchronize((cudaStream_t)stream));
+      return;
+    }
+    be_index_export(g, out_sizes, (unsigned long long*)bloom_off, bloom_k, bloom_dom, pairs, (cudaStream_t)stream);
+  });
+}
+
+int pbng_wing_decompose(pbng_csr U, pbng_csr V, int side, uint64_t* out_theta, uint64_t* out_info, void* stream) {
+  return guarded([&] {
+    Dev g;
+    orient(U, V, side, g);
+    if (out_info) std::memset(out_info, 0, 4 * sizeof(uint64_t));
+    if (!out_theta && g.m) fail(PBNG_ERR_ARG, "out_theta is null");
+    if (g.m == 0) return;
+    wing_decompose(g, out_theta, out_info, (cudaStream_t)stream);
   });
 }
 

@@ -31,7 +31,7 @@ import oracle  # noqa: E402
 def main():
     cfg = sys.argv[1]
     src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
-    cache = os.environ.get("PBNG_CACHE", "/root/cert")
+    cache = os.environ.get("PBNG_CACHE", os.path.join(ROOT, "data"))
     info = json.load(open(os.path.join(src, f"theta_cfg{cfg}.json")))
     vals = np.load(os.path.join(src, f"theta_cfg{cfg}_values.npy"))
     idx = np.concatenate([np.frombuffer(lzma.decompress(open(os.path.join(src, f"theta_cfg{cfg}_part{p}.xz"), "rb")
