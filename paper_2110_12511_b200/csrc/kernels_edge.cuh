@@ -19,7 +19,7 @@
 // CSR order by k_edge_gather.
 //
 // Tiers by the start's wedge bound pb = Σ_mid cutM[mid]:
-//   W  cap <= kEdgeWarpPb    warp per start, per-warp smem hash (1024 slots)
+//   W  cap <= kEdgeWarpPb    warp per start, per-warp smem hash (512 slots)
 //   C  cap <= kEdgeCtaPb     CTA per start, CTA smem hash (8192 slots)
 //   D  larger                persistent CTA per start: dense counters over the
 //                            last ids (< start id) in shared memory when the
@@ -41,7 +41,7 @@
 namespace pbng {
 
 #ifndef PBNG_EDGE_WARP_PB
-#define PBNG_EDGE_WARP_PB 512
+#define PBNG_EDGE_WARP_PB 256
 #endif
 #ifndef PBNG_EDGE_CTA_PB
 #define PBNG_EDGE_CTA_PB 4096
@@ -50,7 +50,7 @@ namespace pbng {
 #define PBNG_EDGE_DENSE_SMEM 49152
 #endif
 constexpr uint32_t kEdgeWarpPb = PBNG_EDGE_WARP_PB;  // test builds lower the tier bounds
-constexpr uint32_t kEdgeWarpLog = 10;         // 1024 slots per warp
+constexpr uint32_t kEdgeWarpLog = 9;          // 512 slots per warp: 5 CTAs of 8 warps per SM
 constexpr uint32_t kEdgeWarpThreads = 256;
 constexpr uint32_t kEdgeCtaPb = PBNG_EDGE_CTA_PB;
 constexpr uint32_t kEdgeCtaLog = 13;          // 8192 slots (+ filled-slot list): two CTAs per SM
@@ -59,6 +59,9 @@ constexpr uint32_t kEdgeDenseSmem = PBNG_EDGE_DENSE_SMEM;  // dense smem counter
 constexpr uint32_t kEdgeDenseThreads = 1024;
 constexpr uint32_t kEdgeBigLog = 14;          // tier-D shared hash: 16384 slots, <= 8192 keys
 constexpr uint32_t kEdgeBigCap = PBNG_EDGE_CTA_PB * 2;
+// shared words of the tier-D tables (dense counters or hash + filled list)
+constexpr uint32_t kEdgeDenseWords = kEdgeDenseSmem > 2 * (1u << kEdgeBigLog) + kEdgeBigCap
+                                         ? kEdgeDenseSmem : 2 * (1u << kEdgeBigLog) + kEdgeBigCap;
 
 struct EdgeArgs {
   uint32_t nS;
@@ -72,6 +75,7 @@ struct EdgeArgs {
   uint2* q;                           // tier queues: q[t * nS + i] = (start, cap)
   uint32_t* nq;                       // [3] queue lengths, [3] tier-D ticket
   unsigned long long* wedges;         // Alg.1 wedges expanded (pass 1), may be null
+  uint32_t* plen;                     // per start-side edge: prefix length (written by k_edge_classify)
   uint32_t* dense;                    // tier-D global counters, nS per CTA
 };
 
@@ -137,9 +141,8 @@ __device__ __forceinline__ uint64_t edge_walk(const EdgeArgs& a, uint32_t s, uin
     uint32_t len = 0;
     uint64_t base = 0;
     if (e < e1) {
-      const uint32_t mid = a.adjS[e];
-      base = a.offM[mid];
-      len = edge_lower_bound(a.adjM + base, a.cutM[mid], s);  // ranked above mid and below s
+      len = a.plen[e];  // ranked above mid and below s (k_edge_classify)
+      if (len) base = a.offM[a.adjS[e]];
     }
     uint32_t incl = len;
 #pragma unroll
@@ -191,9 +194,82 @@ __device__ __forceinline__ uint64_t edge_walk(const EdgeArgs& a, uint32_t s, uin
   return walked;
 }
 
+// Same passes with the whole CTA flattened over the wedges: mids are taken
+// blockDim at a time (one per thread: prefix length by binary search, block
+// scan), then every thread takes wedges t, t + blockDim, ... of the chunk and
+// finds its mid by binary search over the scanned lengths, so a start with a
+// few long prefixes keeps every warp busy.  Pass-2 sums per mid are combined
+// in shared memory and added to accS once per mid.  Contains __syncthreads.
+struct EdgeCtaScratch {
+  uint32_t pre[kEdgeDenseThreads];
+  unsigned long long base[kEdgeDenseThreads];
+  unsigned long long sum[kEdgeDenseThreads];
+  uint32_t scan[33];
+};
+template <int PASS, class Tab>
+__device__ __forceinline__ uint64_t edge_walk_cta(const EdgeArgs& a, uint32_t s, Tab& t, EdgeCtaScratch& sc) {
+  const uint64_t e0 = a.offS[s], e1 = a.offS[s + 1];
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  uint64_t walked = 0;
+  for (uint64_t c = e0; c < e1; c += nt) {
+    const uint32_t nd = (uint32_t)(e1 - c < nt ? e1 - c : nt);
+    uint32_t len = 0;
+    uint64_t base = 0;
+    if (tid < nd) {
+      len = a.plen[c + tid];
+      if (len) base = a.offM[a.adjS[c + tid]];
+    }
+    uint32_t total;
+    const uint32_t pre = block_excl_scan(len, sc.scan, &total);
+    if (tid < nd) {
+      sc.pre[tid] = pre;
+      sc.base[tid] = base;
+      if (PASS == 2) sc.sum[tid] = 0;
+    }
+    __syncthreads();
+    walked += total;
+    for (uint32_t k = tid; k < total; k += nt) {
+      uint32_t lo = 0, hi = nd;  // largest j with pre[j] <= k
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sc.pre[mid] <= k) lo = mid; else hi = mid;
+      }
+      const uint64_t f = sc.base[lo] + (k - sc.pre[lo]);
+      const uint32_t last = a.adjM[f];
+      PBNG_DCHECK(last < s);
+      if (PASS == 1) t.add(last);
+      if (PASS == 2) {
+        const uint32_t cw = t.get(last);
+        if (cw >= 2) {
+          red_add_u64(a.accM + f, (uint64_t)(cw - 1));
+          atomicAdd(&sc.sum[lo], (unsigned long long)(cw - 1));
+        }
+      }
+      if (PASS == 3) t.clear(last);
+    }
+    __syncthreads();
+    if (PASS == 2 && tid < nd && sc.sum[tid]) a.accS[c + tid] += sc.sum[tid];
+  }
+  return walked;
+}
+
+template <class Tab>
+__device__ __forceinline__ uint64_t edge_start_cta(const EdgeArgs& a, uint32_t s, Tab& t, EdgeCtaScratch& sc) {
+  const uint64_t walked = edge_walk_cta<1>(a, s, t, sc);
+  __syncthreads();
+  edge_walk_cta<2>(a, s, t, sc);
+  __syncthreads();
+  if (Tab::kRewalk) {
+    edge_walk_cta<3>(a, s, t, sc);
+    __syncthreads();
+  }
+  return walked;
+}
+
 // Route every start by its exact Alg.1 wedge count pb = Σ_mid |prefix(mid, s)|
-// (warp per start, lanes over mids, one binary search per mid); the table a
-// start needs holds at most cap = min(pb, s) distinct lasts (ids below s).
+// (warp per start, lanes over mids, one binary search per mid, whose result
+// is kept in plen for the walks); the table a start needs holds at most
+// cap = min(pb, s) distinct lasts (ids below s).
 __global__ void __launch_bounds__(256) k_edge_classify(EdgeArgs a) {
   const uint32_t ln = lane_id();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -204,7 +280,9 @@ __global__ void __launch_bounds__(256) k_edge_classify(EdgeArgs a) {
     uint64_t pb = 0;
     for (uint64_t e = e0 + ln; e < e1; e += 32) {
       const uint32_t mid = a.adjS[e];
-      pb += edge_lower_bound(a.adjM + a.offM[mid], a.cutM[mid], (uint32_t)x);
+      const uint32_t len = edge_lower_bound(a.adjM + a.offM[mid], a.cutM[mid], (uint32_t)x);
+      a.plen[e] = len;
+      pb += len;
     }
     pb = warp_sum(pb);
     if (ln == 0 && pb >= 2) {
@@ -270,10 +348,9 @@ __global__ void __launch_bounds__(kEdgeWarpThreads) k_edge_warp(EdgeArgs a) {
 // Tier C: CTA per start.
 __global__ void __launch_bounds__(kEdgeCtaThreads) k_edge_cta(EdgeArgs a) {
   extern __shared__ uint32_t sm[];
-  __shared__ unsigned long long s_sum[kEdgeCtaThreads / 32][32];
   __shared__ uint32_t s_n;
-  const uint32_t w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t T = 1u << kEdgeCtaLog;
+  EdgeCtaScratch& sc = *reinterpret_cast<EdgeCtaScratch*>(sm + 2 * T + kEdgeCtaPb);
   EdgeHash h{sm, sm + T, sm + 2 * T, &s_n, kEdgeCtaLog};
   for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
     h.keys[i] = kEmpty;
@@ -284,13 +361,13 @@ __global__ void __launch_bounds__(kEdgeCtaThreads) k_edge_cta(EdgeArgs a) {
   const uint32_t n = a.nq[1];
   uint64_t walked = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    walked += edge_start(a, a.q[(uint64_t)a.nS + i].x, w, nw, h, s_sum[w], CtaSync());
+    walked += edge_start_cta(a, a.q[(uint64_t)a.nS + i].x, h, sc);  // every thread sees the total
     h.reset(threadIdx.x, blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
   }
-  if (a.wedges && lane_id() == 0 && walked) atomicAdd(a.wedges, (unsigned long long)walked);
+  if (a.wedges && threadIdx.x == 0 && walked) atomicAdd(a.wedges, (unsigned long long)walked);
 }
 
 // Tier D: persistent CTAs take starts by ticket.  Lasts are ids below s:
@@ -300,15 +377,13 @@ __global__ void __launch_bounds__(kEdgeCtaThreads) k_edge_cta(EdgeArgs a) {
 //                              cleared by a third walk
 __global__ void __launch_bounds__(kEdgeDenseThreads) k_edge_dense(EdgeArgs a) {
   extern __shared__ uint32_t sm[];
-  __shared__ unsigned long long s_sum[kEdgeDenseThreads / 32][32];
   __shared__ uint32_t s_i, s_n;
-  const uint32_t w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t n = a.nq[2];
+  EdgeCtaScratch& sc = *reinterpret_cast<EdgeCtaScratch*>(sm + kEdgeDenseWords);
   uint32_t* gcnt = a.dense + (uint64_t)blockIdx.x * a.nS;
   const uint32_t TB = 1u << kEdgeBigLog;
   EdgeHash h{sm, sm + TB, sm + 2 * TB, &s_n, kEdgeBigLog};
   bool hash_ready = false;
-  auto sync = CtaSync();
   uint64_t walked = 0;
   for (;;) {
     if (threadIdx.x == 0) s_i = atomicAdd(&a.nq[3], 1u);
@@ -323,7 +398,7 @@ __global__ void __launch_bounds__(kEdgeDenseThreads) k_edge_dense(EdgeArgs a) {
       for (uint32_t j = threadIdx.x; j < s; j += blockDim.x) sm[j] = 0;
       hash_ready = false;
       __syncthreads();
-      walked += edge_start(a, s, w, nw, t, s_sum[w], sync);
+      walked += edge_start_cta(a, s, t, sc);
     } else if (qe.y <= kEdgeBigCap) {
       if (!hash_ready) {
         for (uint32_t j = threadIdx.x; j < TB; j += blockDim.x) {
@@ -334,17 +409,17 @@ __global__ void __launch_bounds__(kEdgeDenseThreads) k_edge_dense(EdgeArgs a) {
         hash_ready = true;
         __syncthreads();
       }
-      walked += edge_start(a, s, w, nw, h, s_sum[w], sync);
+      walked += edge_start_cta(a, s, h, sc);
       h.reset(threadIdx.x, blockDim.x);
       __syncthreads();
       if (threadIdx.x == 0) s_n = 0;
       __syncthreads();
     } else {
       EdgeDenseGlobal t{gcnt};
-      walked += edge_start(a, s, w, nw, t, s_sum[w], sync);
+      walked += edge_start_cta(a, s, t, sc);
     }
   }
-  if (a.wedges && lane_id() == 0 && walked) atomicAdd(a.wedges, (unsigned long long)walked);
+  if (a.wedges && threadIdx.x == 0 && walked) atomicAdd(a.wedges, (unsigned long long)walked);
 }
 
 // ⋈_e in the caller's CSR order of the output side: caller edge i = (x, y)

@@ -127,14 +127,14 @@ struct BeSize {
 struct BeAssign {
   const BeArgs* b;
   uint32_t s;
-  uint32_t* s_nb;
-  uint32_t* s_np;
+  unsigned long long* s_acc;  // (blooms << 40) | pairs: one atomic keeps bloom order = pair order
   __device__ __forceinline__ void operator()(uint64_t, uint64_t, uint32_t last) {
     const uint32_t c = __ldcg(&b->cnt[last]);
     if (c < 2) return;
     if (atomicCAS(&b->bidx[last], kBeInvalid, kBeInvalid - 1) != kBeInvalid) return;
-    const uint32_t li = atomicAdd(s_nb, 1u);
-    const uint32_t pb = atomicAdd(s_np, c);
+    const unsigned long long old = atomicAdd(s_acc, (1ull << 40) | c);
+    const uint32_t li = (uint32_t)(old >> 40);
+    const uint32_t pb = (uint32_t)(old & ((1ull << 40) - 1));
     const uint64_t bid = b->bS[s] + li;
     b->bloom_off[bid] = b->pS[s] + pb;
     b->bloom_k[bid] = c;
@@ -164,6 +164,7 @@ struct BeFill {
 template <bool FILL>
 __global__ void __launch_bounds__(kBeThreads) k_be_build(BeArgs b) {
   __shared__ uint32_t s_i, s_nb, s_np;
+  __shared__ unsigned long long s_acc;
   const uint32_t w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const EdgeArgs& a = b.a;
   BeArgs* bp = &b;
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kBeThreads) k_be_build(BeArgs b) {
       s_i = atomicAdd(b.ticket, 1u);
       s_nb = 0;
       s_np = 0;
+      s_acc = 0;
     }
     __syncthreads();
     const uint32_t s = s_i;
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kBeThreads) k_be_build(BeArgs b) {
         b.np_s[s] = s_np;
       }
     } else {
-      BeAssign as{bp, s, &s_nb, &s_np};
+      BeAssign as{bp, s, &s_acc};
       be_walk(a, s, w, nw, as);
       __syncthreads();
       BeFill fl{bp, s};

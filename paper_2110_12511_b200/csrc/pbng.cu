@@ -58,10 +58,8 @@ size_t win_smem() { return sizeof(WinSmem); }
 size_t hist_smem() { return (size_t)kBins * 12; }
 size_t hash_smem() { return sizeof(HashSmem); }
 size_t edge_warp_smem() { return (size_t)(kEdgeWarpThreads / 32) * (2 * (1u << kEdgeWarpLog) + kEdgeWarpPb) * 4; }
-size_t edge_cta_smem() { return ((size_t)2 * (1u << kEdgeCtaLog) + kEdgeCtaPb) * 4; }
-size_t edge_dense_smem() {
-  return std::max<size_t>((size_t)kEdgeDenseSmem, (size_t)2 * (1u << kEdgeBigLog) + kEdgeBigCap) * 4;
-}
+size_t edge_cta_smem() { return ((size_t)2 * (1u << kEdgeCtaLog) + kEdgeCtaPb) * 4 + sizeof(EdgeCtaScratch); }
+size_t edge_dense_smem() { return (size_t)kEdgeDenseWords * 4 + sizeof(EdgeCtaScratch); }
 size_t fd_smem() { return ((size_t)(kFdThreads / 32) * 2 * kFdWarpSlots + 2 * kFdCtaSlots + kFdThreads) * 4; }
 
 // Per-device one-time setup: the dynamic shared-memory opt-ins (they apply to
@@ -1320,6 +1318,7 @@ void edge_count(const Dev& g, uint64_t* out, uint64_t* out_info, cudaStream_t s)
   CK(cudaMemsetAsync(accV, 0, g.m * 8, r.st));
   const uint32_t nmax = std::max(g.nU, g.nV);
   uint2* q = r.alloc<uint2>(3ull * nmax);
+  uint32_t* plen = r.alloc<uint32_t>(g.m);
   uint32_t* nq = r.alloc<uint32_t>(4);
   uint32_t* dense = nullptr;
   uint32_t ndense = 0;
@@ -1336,6 +1335,7 @@ void edge_count(const Dev& g, uint64_t* out, uint64_t* out_info, cudaStream_t s)
     a.q = q;
     a.nq = nq;
     a.wedges = cnt + 1;
+    a.plen = plen;
     a.dense = nullptr;
     if (a.nS == 0) continue;
     CK(cudaMemsetAsync(nq, 0, 16, r.st));
@@ -1348,7 +1348,7 @@ void edge_count(const Dev& g, uint64_t* out, uint64_t* out_info, cudaStream_t s)
     for (int t = 0; t < 3; t++) info[1 + t] += hq[t];
     if (hq[0]) {
       r.pre(PBNG_K_EDGE);
-      k_edge_warp<<<std::min<uint32_t>(r.nsm * 3, (hq[0] + 7) / 8), kEdgeWarpThreads, edge_warp_smem(), r.st>>>(a);
+      k_edge_warp<<<std::min<uint32_t>(r.nsm * 5, (hq[0] + 7) / 8), kEdgeWarpThreads, edge_warp_smem(), r.st>>>(a);
       r.post(PBNG_K_EDGE);
     }
     if (hq[1]) {
