@@ -252,12 +252,13 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
                                          uint64_t wb, uint64_t a, uint64_t b, const uint32_t* __restrict__ partner,
                                          WinSmem& S, WinShared& sh, Fn& fn, uint32_t chunk = kWinChunk,
                                          const uint32_t* __restrict__ sub = nullptr, uint32_t sj = 0,
-                                         uint32_t sstride = 0) {
+                                         uint32_t sstride = 0, unsigned long long* pc = nullptr) {
   // sub (optional): precomputed bounds of list i's sub-window sj at sub[i * sstride + sj]
   const uint32_t tid = threadIdx.x, ln = lane_id();
   bool any = false;
   for (uint64_t bs = 0; bs < nl; bs += kWinLists) {
     const uint32_t nb = (uint32_t)(nl - bs < kWinLists ? nl - bs : kWinLists);
+    const long long tc0 = pc ? clock64() : 0;
     uint32_t nch = 0;
     if (tid < nb) {
       const uint64_t i = bs + tid;
@@ -291,6 +292,7 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
     }
     __syncthreads();
     any |= tot != 0;
+    const long long tc1 = pc ? clock64() : 0;
     for (;;) {
       uint32_t c = 0;
       if (ln == 0) c = atomicAdd(&sh.next, 1u);
@@ -307,6 +309,11 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
       fn(i0, i0 + chunk < i1e ? i0 + chunk : i1e, e0 + bs + lo);
     }
     __syncthreads();
+    if (pc && tid == 0) {
+      atomicAdd(&pc[6], (unsigned long long)(tc1 - tc0));
+      atomicAdd(&pc[7], (unsigned long long)(clock64() - tc1));
+      atomicAdd(&pc[5], (unsigned long long)nb);
+    }
   }
   return any;
 }
@@ -327,6 +334,10 @@ constexpr uint32_t kWinMaxW = PBNG_WIN_MAX_W;  // windows whose entry counts are
 // appends the word to the touched list (kept in the repeat table's memory,
 // which dense mode does not use), so the sweep visits touched words only.
 constexpr uint32_t kTouchCap = kWinDupSlots * 2;
+// dense sweep: queued hit words per warp; the queues take the shared memory from the
+// repeat table up to the segment tables, all scratch that is refilled before its next use
+constexpr uint32_t kSweepQ = (uint32_t)((offsetof(WinSmem, scan) - offsetof(WinSmem, dup)) / 8) / (kWinThreads / 32);
+static_assert(kSweepQ >= 64 && offsetof(WinSmem, dup) % 8 == 0, "dense sweep queue: a warp appends up to 64 words between drains");
 __device__ __forceinline__ uint32_t dense_log_bits(uint64_t nl) {
   return nl < 4 ? 1u : nl < 16 ? 2u : nl < 256 ? 3u : nl < 65536 ? 4u : 5u;  // log2 of 2..32 bits
 }
@@ -614,6 +625,10 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
     // dense counting in sub-windows of SW ids; with tables, every list's
     // sub-window bounds are found at once (a warp per list, a lane per bound)
     const long long td0 = clock64();
+    if (prof && tid == 0 && pre) {
+      atomicAdd(&cnt->prof3[3], S.ek[kr]);
+      atomicAdd(&cnt->prof3[4], 1ull);
+    }
     const uint32_t NS = (uint32_t)((wb - wa + SW - 1) / SW);
     uint32_t* sub = nullptr;
     if (pre && NS <= 32) {
@@ -627,6 +642,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         }
       }
       __syncthreads();
+      if (prof && tid == 0) atomicAdd(&cnt->prof3[0], (unsigned long long)(clock64() - td0));
     }
     for (uint64_t a = wa; a < wb; a += SW) {
       const uint32_t sj = (uint32_t)((a - wa) / SW);
@@ -650,7 +666,11 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
         dense_mark(partner, i0, i1, (uint32_t)a, skip, lb, mycnt, touch, &sh.ndup);
       };
       const uint32_t chunk = PBNG_DENSE_CHUNK ? PBNG_DENSE_CHUNK : (pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk);
-      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk, sub, sj, 33);
+      const long long tq0 = prof ? clock64() : 0;
+      const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk, sub, sj, 33,
+                                prof ? cnt->prof3 : nullptr);
+      const long long tq1 = prof ? clock64() : 0;
+      if (prof && tid == 0) atomicAdd(&cnt->prof3[1], (unsigned long long)(tq1 - tq0));
       if (!any) continue;
       if (Pass2::kOn) {
         auto sum = [&](uint64_t i0, uint64_t i1, uint64_t e) {
@@ -690,30 +710,56 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
           }
         }
       } else {
+        // Words holding a field >= 2 are rare (a few percent), so emitting straight
+        // from the scan leaves one or two lanes of a warp active per emit (measured:
+        // the sweep took 36% of the dense cycles, issue-bound on that divergence).
+        // Each warp instead queues its hit words (ballot-compacted, kSweepQ) and
+        // drains the queue a word per lane.
         uint4* b4 = reinterpret_cast<uint4*>(S.bits);
-        for (uint32_t t = tid; t < (nwords + 3) >> 2; t += bd) {
-          uint4 v = b4[t];
-          for (uint32_t r = 1; r < R; r++) {
-            const uint4 y = b4[r * (stride >> 2) + t];
-            if (y.x | y.y | y.z | y.w) {
-              b4[r * (stride >> 2) + t] = make_uint4(0, 0, 0, 0);
-              v.x += y.x;
-              v.y += y.y;
-              v.z += y.z;
-              v.w += y.w;
-            }
+        uint2* q = reinterpret_cast<uint2*>(S.dup) + wid * kSweepQ;
+        uint32_t nq = 0;
+        const uint32_t n4 = (nwords + 3) >> 2;
+        auto drain = [&]() {
+          __syncwarp();
+          for (uint32_t i = ln; i < nq; i += 32) {
+            const uint2 e = q[i];
+            sweep_word(e.x, e.y);
           }
-          if (v.x | v.y | v.z | v.w) {
-            b4[t] = make_uint4(0, 0, 0, 0);
-            sweep_word(4 * t, v.x);
-            sweep_word(4 * t + 1, v.y);
-            sweep_word(4 * t + 2, v.z);
-            sweep_word(4 * t + 3, v.w);
+          nq = 0;
+          __syncwarp();
+        };
+        for (uint32_t t0 = wid * 32; t0 < n4; t0 += bd) {
+          const uint32_t t = t0 + ln;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (t < n4) {
+            v = b4[t];
+            for (uint32_t r = 1; r < R; r++) {
+              const uint4 y = b4[r * (stride >> 2) + t];
+              if (y.x | y.y | y.z | y.w) {
+                b4[r * (stride >> 2) + t] = make_uint4(0, 0, 0, 0);
+                v.x += y.x;
+                v.y += y.y;
+                v.z += y.z;
+                v.w += y.w;
+              }
+            }
+            if (v.x | v.y | v.z | v.w) b4[t] = make_uint4(0, 0, 0, 0);
+          }
+          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (uint32_t c = 0; c < 4; c++) {
+            if ((c & 1) == 0 && nq > kSweepQ - 64) drain();
+            const bool hit = (vv[c] & ~lows) != 0;
+            const uint32_t hm = __ballot_sync(kFull, hit);
+            if (hit) q[nq + __popc(hm & lanemask_lt())] = make_uint2(4 * t + c, vv[c]);
+            nq += __popc(hm);
           }
         }
+        drain();
       }
       if (tid == 0) atomicAdd(&dbg[2], 1ull);
       __syncthreads();
+      if (prof && tid == 0) atomicAdd(&cnt->prof3[2], (unsigned long long)(clock64() - tq1));
     }
     // the repeat table's memory held touched words: empty it again
     for (uint32_t i = tid; i < kWinDupSlots; i += bd) S.dup[i] = kEmptySlot;

@@ -70,6 +70,8 @@ struct Counters {
   unsigned long long prof[4];         // tier-2 clock64 of CTA thread 0: starts with tables, precompute, bitmap windows, dense passes
   unsigned long long prof2[4];        // tier-2: cycles / count of starts without tables, count of starts with tables, -
   unsigned long long hashc[4];        // tier 1: starts, starts split into groups, groups, starts passed on to tier 2
+  unsigned long long prof3[8];        // tier-2 dense windows (PBNG_TRACE): cycles of sub-bound tables, marking, sweep;
+                                      // entries, windows, Σ lists per pass; marking set-up cycles, marking loop cycles
 };
 
 // ---------------------------------------------------------------- init
@@ -139,9 +141,13 @@ __global__ void k_classify(uint32_t nU, const uint32_t* __restrict__ list, const
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long wsum = 0, ssum = 0, tw[3] = {0, 0, 0};
-  for (uint64_t b = gw * 32; b < n; b += nw * 32) {
+  // a warp takes G <= 32 vertices at a time: with fewer than 32 vertices per warp in
+  // the batch (late CD iterations) G shrinks, so that every warp gets some and the
+  // serial chain of dependent loads (adjU -> ld) per warp is as short as the batch allows
+  const uint32_t G = n >= nw * 32 ? 32u : (uint32_t)max((unsigned long long)((n + nw - 1) / nw), 1ull);
+  for (uint64_t b = gw * G; b < n; b += nw * G) {
     const uint64_t idx = b + ln;
-    bool ok = idx < n;
+    bool ok = ln < G && idx < n;
     const uint32_t u = ok ? (list ? list[idx] : (uint32_t)idx) : 0u;
     if (ok && !list && part[u] != kUnassigned) ok = false;
     const uint64_t e0 = ok ? offU[u] : 0, d0 = ok ? offU[u + 1] - e0 : 0;

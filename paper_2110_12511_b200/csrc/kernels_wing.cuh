@@ -420,6 +420,161 @@ __global__ void k_wing_update(WingArgs w, uint32_t n, unsigned long long k) {
   }
 }
 
+// ---------------------------------------------------------------- device-driven peel
+// The whole peel in ONE persistent launch (one CTA per SM, co-resident by a
+// cooperative launch): the phases of the host-driven loop above, separated by a
+// grid barrier instead of a kernel boundary and a counter read-back.  Config 3
+// runs 147,592 rounds of a few dozen edges each; host-driven, every round costs
+// three launches and two stream synchronisations (~0.2 ms), here two grid
+// barriers.  Counters are double-buffered so that a counter is reset only in a
+// phase in which no thread reads or adds to it:
+//   cnt[2]  lengths of the S / X lists (SX[cs] is peeled, SX[cs^1] collects the
+//           crossers); nT[2] touched blooms of round r in nT[r & 1].
+struct WingDev {
+  uint32_t cnt[2];
+  uint32_t nT[2];
+  uint32_t nlive;
+  uint32_t pad;
+  unsigned long long minsup;
+  unsigned long long bar;      // grid barrier: arrivals so far (monotonic)
+  unsigned long long levels, rounds;
+};
+constexpr uint32_t kWingThreads = 1024;
+
+__device__ __forceinline__ void wing_grid_sync(unsigned long long* bar, unsigned long long& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    epoch += gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    while (*(volatile unsigned long long*)bar < epoch) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint32_t* live0, uint32_t* live1,
+                                                                  uint32_t* sx0, uint32_t* sx1, WingDev* c) {
+  const uint32_t ln = lane_id();
+  const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t gw = gt >> 5, nw = nt >> 5;
+  const bool lead = gt == 0;
+  unsigned long long epoch = 0, k = 0, levels = 0, rounds = 0;
+  uint32_t* live[2] = {live0, live1};
+  uint32_t* SX[2] = {sx0, sx1};
+  uint32_t nlive = (uint32_t)w.m, cur = 0;
+  for (;;) {
+    // --- level scan: compact the live list, minimum live support
+    {
+      const uint32_t* in = live[cur];
+      uint32_t* out = live[cur ^ 1];
+      unsigned long long mn = ~0ull;
+      for (uint64_t i0 = gt - ln; i0 < nlive; i0 += nt) {
+        const uint64_t i = i0 + ln;
+        bool keep = false;
+        uint32_t e = 0;
+        if (i < nlive) {
+          e = __ldcg(in + i);
+          keep = __ldcg(w.alive + e);
+          if (keep) mn = min(mn, __ldcg(w.sup + e));
+        }
+        warp_append(keep, e, out, &c->nlive);
+      }
+      mn = warp_min_u64(mn);
+      if (ln == 0 && mn != ~0ull) atomicMin(&c->minsup, mn);
+    }
+    wing_grid_sync(&c->bar, epoch);
+    cur ^= 1;
+    nlive = *(volatile uint32_t*)&c->nlive;
+    if (nlive == 0) break;
+    k = max(k, *(volatile unsigned long long*)&c->minsup);
+    levels++;
+    // --- S = live edges with support <= k
+    for (uint64_t i0 = gt - ln; i0 < nlive; i0 += nt) {
+      const uint64_t i = i0 + ln;
+      bool take = false;
+      uint32_t e = 0;
+      if (i < nlive) {
+        e = __ldcg(live[cur] + i);
+        take = __ldcg(w.sup + e) <= k;  // every listed edge is alive (the scan dropped the peeled ones)
+      }
+      warp_append(take, e, SX[0], &c->cnt[0]);
+    }
+    wing_grid_sync(&c->bar, epoch);
+    if (lead) {  // every thread read them before the barrier above
+      c->nlive = 0;
+      c->minsup = ~0ull;
+    }
+    uint32_t cs = 0;
+    bool any = false;
+    for (;;) {
+      const uint32_t nS = *(volatile uint32_t*)&c->cnt[cs];
+      if (nS == 0) break;
+      any = true;
+      const uint32_t r = (uint32_t)(rounds & 1);
+      rounds++;
+      // --- claim (k_wing_claim) + kill: the claim reads no `alive`, so S leaves here
+      if (lead) c->nT[r ^ 1] = 0;
+      const uint32_t* S = SX[cs];
+      for (uint64_t i = gw; i < nS; i += nw) {
+        const uint32_t e = __ldcg(S + i);
+        if (ln == 0) {
+          w.theta[e] = k;
+          w.alive[e] = 0;
+        }
+        for (uint64_t j = w.inc_off[e] + ln; j < w.inc_off[e + 1]; j += 32) {
+          const uint32_t p = w.inc[j];
+          if (__ldcg(w.pstate + p) != 0 || atomicCAS(&w.pstate[p], 0u, 1u) != 0u) continue;
+          const uint32_t b = w.pair_bloom[p];
+          if (atomicAdd(&w.bloom_d[b], 1u) == 0) w.T[atomicAdd(&c->nT[r], 1u)] = b;
+        }
+      }
+      wing_grid_sync(&c->bar, epoch);
+      // --- batch bloom update (k_wing_update); crossers go to SX[cs ^ 1]
+      const uint32_t nT = *(volatile uint32_t*)&c->nT[r];
+      if (lead) c->cnt[cs] = 0;
+      uint32_t* X = SX[cs ^ 1];
+      uint32_t* nX = &c->cnt[cs ^ 1];
+      auto dec = [&](uint32_t x, unsigned long long d) {
+        const unsigned long long old = atomicAdd(&w.sup[x], (unsigned long long)(0ull - d));
+        if (old > k && old - d <= k) X[atomicAdd(nX, 1u)] = x;
+      };
+      for (uint64_t i = gw; i < nT; i += nw) {
+        const uint32_t b = __ldcg(w.T + i);
+        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
+        for (uint64_t p = w.bloom_off[b] + ln; p < w.bloom_off[b + 1]; p += 32) {
+          const uint32_t st = __ldcg(w.pstate + p);
+          if (st == 2) continue;
+          const uint2 pr = w.pair[p];
+          if (st == 1) {
+            if (kb > 1) {
+              if (__ldcg(w.alive + pr.x)) dec(pr.x, kb - 1);
+              if (__ldcg(w.alive + pr.y)) dec(pr.y, kb - 1);
+            }
+            w.pstate[p] = 2;
+          } else {
+            dec(pr.x, d);
+            dec(pr.y, d);
+          }
+        }
+        __syncwarp();
+        if (ln == 0) {
+          w.bloom_k[b] = kb - d;
+          w.bloom_d[b] = 0;
+        }
+      }
+      wing_grid_sync(&c->bar, epoch);
+      cs ^= 1;
+    }
+    if (!any) wing_grid_sync(&c->bar, epoch);  // (cannot happen: the minimum is selected) keeps the reset ordered
+  }
+  if (lead) {
+    c->levels = levels;
+    c->rounds = rounds;
+  }
+}
+
 // θ back to the caller's CSR order (positions found as in k_edge_gather)
 __global__ void k_wing_gather(uint32_t nX, uint64_t m, const uint64_t* __restrict__ offX,
                               const uint32_t* __restrict__ idxX, const uint32_t* __restrict__ rankX,

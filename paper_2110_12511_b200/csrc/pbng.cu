@@ -939,6 +939,9 @@ void run_cd(Run& r, State& S, uint32_t P, uint32_t opts, Plan& plan, pbng_stats&
     std::fprintf(stderr, "tier2 cycles: tabled_starts=%llu precompute=%llu bitmap=%llu dense=%llu | untabled=%llu "
                  "n_untabled=%llu n_tabled=%llu | windows=%llu over=%llu dense_passes=%llu\n", hc.prof[0], hc.prof[1],
                  hc.prof[2], hc.prof[3], hc.prof2[0], hc.prof2[1], hc.prof2[2], hc.dbg[0], hc.dbg[1], hc.dbg[2]);
+    std::fprintf(stderr, "tier2 dense: subtab=%llu mark=%llu sweep=%llu | entries=%llu windows=%llu lists_per_batch_sum=%llu "
+                 "| mark_setup=%llu mark_loop=%llu\n", hc.prof3[0], hc.prof3[1], hc.prof3[2], hc.prof3[3], hc.prof3[4],
+                 hc.prof3[5], hc.prof3[6], hc.prof3[7]);
     for (const TraceRow& t : rows)
       std::fprintf(stderr, "cd pid=%u nF=%u tiers=%u/%u/%u wedges=%llu w2cum=%llu recount=%d ms=%.3f agg_ms=%.3f "
                    "idspace=%u split=%u\n", t.pid, t.nF, t.t0, t.t1, t.t2, t.wedges, t.w2cum, (int)t.recount,
@@ -1538,6 +1541,29 @@ void wing_peel(Run& r, const Dev& gr, const BeIndex& I, uint64_t* theta, uint64_
   r.post(PBNG_K_FD);
   uint32_t* SX[2] = {r.alloc<uint32_t>(m), r.alloc<uint32_t>(m)};
   w.T = r.alloc<uint32_t>(std::max<uint64_t>(I.nb, 1));
+  if (!std::getenv("PBNG_WING_HOST")) {
+    // device-driven peel: one persistent cooperative launch (k_wing_peel);
+    // PBNG_WING_HOST=1 keeps the host-driven rounds below (same phases, for A/B runs)
+    WingDev* dc = r.alloc<WingDev>(1);
+    WingDev init;
+    std::memset(&init, 0, sizeof(init));
+    init.minsup = ~0ull;
+    CK(cudaMemcpyAsync(dc, &init, sizeof(init), cudaMemcpyHostToDevice, r.st));
+    void* args[] = {&w, &live[0], &live[1], &SX[0], &SX[1], &dc};
+    r.pre(PBNG_K_FD);
+    CK(cudaLaunchCooperativeKernel((const void*)k_wing_peel, dim3(r.nsm), dim3(kWingThreads), args, 0, r.st));
+    r.post(PBNG_K_FD);
+    WingDev out;
+    CK(cudaMemcpyAsync(&out, dc, sizeof(out), cudaMemcpyDeviceToHost, r.st));
+    CK(cudaStreamSynchronize(r.st));
+    if (info) {
+      info[0] = I.nb;
+      info[1] = I.np;
+      info[2] = out.levels;
+      info[3] = out.rounds;
+    }
+    return;
+  }
   w.ctl = r.alloc<WingCtl>(1);
   WingCtl* hctl = nullptr;
   CK(cudaMallocHost(&hctl, sizeof(WingCtl)));

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--opts", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--count-only", action="store_true")
+    ap.add_argument("--sha", action="store_true", help="also print SHA-256 of θ (caller labels)")
     args = ap.parse_args()
     entry.build()
     import paper_2110_12511_b200 as pb
@@ -38,9 +39,12 @@ def main():
             pb.pbng_count_butterflies(d)
             st = {}
         else:
-            _, st = pb.pbng_tip_decompose(d, P, opts=args.opts)
+            tip, st = pb.pbng_tip_decompose(d, P, opts=args.opts)
         e1.record()
         torch.cuda.synchronize()
+        if args.sha and not args.count_only:
+            import hashlib
+            st = dict(st, theta_sha256=hashlib.sha256(pb.as_u64(tip).tobytes()).hexdigest())
         print(json.dumps({"rep": r, "ms": e0.elapsed_time(e1), **st}), flush=True)
 
 

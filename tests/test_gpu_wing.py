@@ -109,3 +109,20 @@ def test_wing_configs(pb, cfg):
     th, info = pb.pbng_wing_decompose(dev(pb, g))
     assert np.array_equal(pb.as_u64(th), oracle.bup_wing(g)), info
     assert info["levels"] >= 1 and info["rounds"] >= info["levels"]
+
+
+def test_wing_host_driven_rounds(pb, monkeypatch):
+    """The host-driven round loop (PBNG_WING_HOST=1: one launch per phase) and the
+    device-driven peel (k_wing_peel, one persistent cooperative launch, the default) run the
+    same phases: same θ_e, levels and rounds, both bit-exact against Alg.2 BUP."""
+    for g in list(tiny_corpus(40, 777)) + [gg.config(1)[0], gg.config(2)[0]]:
+        d = dev(pb, g)
+        want = oracle.bup_wing(g)
+        monkeypatch.delenv("PBNG_WING_HOST", raising=False)
+        th_d, info_d = pb.pbng_wing_decompose(d)
+        monkeypatch.setenv("PBNG_WING_HOST", "1")
+        th_h, info_h = pb.pbng_wing_decompose(d)
+        monkeypatch.delenv("PBNG_WING_HOST", raising=False)
+        assert np.array_equal(pb.as_u64(th_d), want), g.name
+        assert np.array_equal(pb.as_u64(th_h), want), g.name
+        assert info_d["levels"] == info_h["levels"] and info_d["rounds"] == info_h["rounds"], (info_d, info_h)
