@@ -440,6 +440,8 @@ struct WingDev {
   unsigned long long levels, rounds;
 };
 constexpr uint32_t kWingThreads = 1024;
+constexpr uint32_t kWingBigLen = 512;   // pair lists longer than this are walked by a whole CTA
+constexpr uint32_t kWingBigCap = 256;   // ... up to this many per CTA and phase (more: the warp walks them)
 
 __device__ __forceinline__ void wing_grid_sync(unsigned long long* bar, unsigned long long& epoch) {
   __syncthreads();
@@ -464,6 +466,8 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
   uint32_t* live[2] = {live0, live1};
   uint32_t* SX[2] = {sx0, sx1};
   uint32_t nlive = (uint32_t)w.m, cur = 0;
+  __shared__ uint32_t big[kWingBigCap];  // per CTA: long pair lists left to the whole CTA
+  __shared__ uint32_t nbig;
   for (;;) {
     // --- level scan: compact the live list, minimum live support
     {
@@ -517,18 +521,38 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       // --- claim (k_wing_claim) + kill: the claim reads no `alive`, so S leaves here
       if (lead) c->nT[r ^ 1] = 0;
       const uint32_t* S = SX[cs];
+      auto claim = [&](uint64_t j) {
+        const uint32_t p = w.inc[j];
+        if (__ldcg(w.pstate + p) != 0 || atomicCAS(&w.pstate[p], 0u, 1u) != 0u) return;
+        const uint32_t b = w.pair_bloom[p];
+        if (atomicAdd(&w.bloom_d[b], 1u) == 0) w.T[atomicAdd(&c->nT[r], 1u)] = b;
+      };
+      if (threadIdx.x == 0) nbig = 0;
+      __syncthreads();
       for (uint64_t i = gw; i < nS; i += nw) {
         const uint32_t e = __ldcg(S + i);
         if (ln == 0) {
           w.theta[e] = k;
           w.alive[e] = 0;
         }
-        for (uint64_t j = w.inc_off[e] + ln; j < w.inc_off[e + 1]; j += 32) {
-          const uint32_t p = w.inc[j];
-          if (__ldcg(w.pstate + p) != 0 || atomicCAS(&w.pstate[p], 0u, 1u) != 0u) continue;
-          const uint32_t b = w.pair_bloom[p];
-          if (atomicAdd(&w.bloom_d[b], 1u) == 0) w.T[atomicAdd(&c->nT[r], 1u)] = b;
+        const uint64_t j0 = w.inc_off[e], j1 = w.inc_off[e + 1];
+        // an edge in many pairs is left to the whole CTA (below): a warp walking
+        // 10^4..10^5 pairs alone would set the length of the round
+        uint32_t slot = kWingBigCap;
+        if (j1 - j0 > kWingBigLen) {
+          if (ln == 0) slot = atomicAdd(&nbig, 1u);
+          slot = __shfl_sync(kFull, slot, 0);
+          if (slot < kWingBigCap) {
+            if (ln == 0) big[slot] = e;
+            continue;
+          }
         }
+        for (uint64_t j = j0 + ln; j < j1; j += 32) claim(j);
+      }
+      __syncthreads();
+      for (uint32_t i = 0, n = min(nbig, kWingBigCap); i < n; i++) {
+        const uint32_t e = big[i];
+        for (uint64_t j = w.inc_off[e] + threadIdx.x; j < w.inc_off[e + 1]; j += blockDim.x) claim(j);
       }
       wing_grid_sync(&c->bar, epoch);
       // --- batch bloom update (k_wing_update); crossers go to SX[cs ^ 1]
@@ -540,26 +564,50 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
         const unsigned long long old = atomicAdd(&w.sup[x], (unsigned long long)(0ull - d));
         if (old > k && old - d <= k) X[atomicAdd(nX, 1u)] = x;
       };
+      auto upd_pair = [&](uint64_t p, uint32_t kb, uint32_t d) {
+        const uint32_t st = __ldcg(w.pstate + p);
+        if (st == 2) return;
+        const uint2 pr = w.pair[p];
+        if (st == 1) {
+          if (kb > 1) {
+            if (__ldcg(w.alive + pr.x)) dec(pr.x, kb - 1);
+            if (__ldcg(w.alive + pr.y)) dec(pr.y, kb - 1);
+          }
+          w.pstate[p] = 2;
+        } else {
+          dec(pr.x, d);
+          dec(pr.y, d);
+        }
+      };
+      if (threadIdx.x == 0) nbig = 0;
+      __syncthreads();
       for (uint64_t i = gw; i < nT; i += nw) {
         const uint32_t b = __ldcg(w.T + i);
-        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
-        for (uint64_t p = w.bloom_off[b] + ln; p < w.bloom_off[b + 1]; p += 32) {
-          const uint32_t st = __ldcg(w.pstate + p);
-          if (st == 2) continue;
-          const uint2 pr = w.pair[p];
-          if (st == 1) {
-            if (kb > 1) {
-              if (__ldcg(w.alive + pr.x)) dec(pr.x, kb - 1);
-              if (__ldcg(w.alive + pr.y)) dec(pr.y, kb - 1);
-            }
-            w.pstate[p] = 2;
-          } else {
-            dec(pr.x, d);
-            dec(pr.y, d);
+        const uint64_t p0 = w.bloom_off[b], p1 = w.bloom_off[b + 1];
+        uint32_t slot = kWingBigCap;
+        if (p1 - p0 > kWingBigLen) {  // a large bloom is updated by the whole CTA (below)
+          if (ln == 0) slot = atomicAdd(&nbig, 1u);
+          slot = __shfl_sync(kFull, slot, 0);
+          if (slot < kWingBigCap) {
+            if (ln == 0) big[slot] = b;
+            continue;
           }
         }
+        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
+        for (uint64_t p = p0 + ln; p < p1; p += 32) upd_pair(p, kb, d);
         __syncwarp();
         if (ln == 0) {
+          w.bloom_k[b] = kb - d;
+          w.bloom_d[b] = 0;
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = 0, n = min(nbig, kWingBigCap); i < n; i++) {
+        const uint32_t b = big[i];
+        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
+        for (uint64_t p = w.bloom_off[b] + threadIdx.x; p < w.bloom_off[b + 1]; p += blockDim.x) upd_pair(p, kb, d);
+        __syncthreads();  // every thread has read kb and d
+        if (threadIdx.x == 0) {
           w.bloom_k[b] = kb - d;
           w.bloom_d[b] = 0;
         }
