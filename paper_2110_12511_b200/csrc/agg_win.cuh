@@ -193,44 +193,6 @@ __device__ __forceinline__ void seg_visit(const uint32_t* __restrict__ p, uint64
   }
 }
 
-// seg_visit with the unaligned head and tail and the first body step loaded before any
-// entry is used (one load round trip for a one-step chunk instead of three).  Used by the
-// bitmap windows (chunks of one step, D = 2: bitmap cycles 2.08e11 -> 1.07e11 on config 5);
-// with D = 4 (dense passes) the extra live registers made the kernel slower.
-template <int D = kSegDepth, class Fn>
-__device__ __forceinline__ void seg_visit_pre(const uint32_t* __restrict__ p, uint64_t i0, uint64_t i1, Fn& fn) {
-  const uint32_t ln = lane_id();
-  uint64_t h = (i0 + 3) & ~3ull;  // first 16-byte aligned index
-  if (h > i1) h = i1;
-  const uint64_t t = h + ((i1 - h) & ~3ull);  // end of the aligned body
-  const bool okh = i0 + ln < h, okt = t + ln < i1;
-  const uint32_t xh = okh ? __ldg(p + i0 + ln) : 0u, xt = okt ? __ldg(p + t + ln) : 0u;
-  uint4 v[D];
-  bool ok[D];
-  auto load = [&](uint64_t q0) {
-#pragma unroll
-    for (int j = 0; j < D; j++) {
-      const uint64_t q = q0 + 128 * j + 4 * ln;
-      ok[j] = q < t;
-      v[j] = ok[j] ? __ldg(reinterpret_cast<const uint4*>(p + q)) : make_uint4(0, 0, 0, 0);
-    }
-  };
-  if (h < t) load(h);
-  fn(okh, xh);
-  for (uint64_t q0 = h; q0 < t;) {
-#pragma unroll
-    for (int j = 0; j < D; j++) {
-      fn(ok[j], v[j].x);
-      fn(ok[j], v[j].y);
-      fn(ok[j], v[j].z);
-      fn(ok[j], v[j].w);
-    }
-    q0 += 128 * D;
-    if (q0 < t) load(q0);
-  }
-  fn(okt, xt);
-}
-
 // Mark the entries p[i0, i1) (all inside the window starting at `a`) in the
 // bitmap; repeats go to the table.
 // Lanes of one warp step hold distinct ids of one sorted list, so in dense
@@ -259,7 +221,7 @@ __device__ __forceinline__ void win_mark(const uint32_t* __restrict__ p, uint64_
       if (atomicOr(&S.bits[o >> 5], bit) & bit) win_dup_insert(S, sh, x);
     }
   };
-  seg_visit_pre<D>(p, i0, i1, one);
+  seg_visit<D>(p, i0, i1, one);
 }
 
 // Zero the first nwords words of the window array with 16-byte stores (whole CTA).

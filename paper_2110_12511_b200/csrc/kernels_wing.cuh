@@ -438,6 +438,7 @@ struct WingDev {
   unsigned long long minsup;
   unsigned long long bar;      // grid barrier: arrivals so far (monotonic)
   unsigned long long levels, rounds;
+  unsigned long long clk[4];   // CTA 0 thread 0: cycles in level scans, selects, claim phases, update phases
 };
 constexpr uint32_t kWingThreads = 1024;
 constexpr uint32_t kWingBigLen = 512;   // pair lists longer than this are walked by a whole CTA
@@ -468,6 +469,13 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
   uint32_t nlive = (uint32_t)w.m, cur = 0;
   __shared__ uint32_t big[kWingBigCap];  // per CTA: long pair lists left to the whole CTA
   __shared__ uint32_t nbig;
+  unsigned long long clk[4] = {0, 0, 0, 0};
+  long long tc = clock64();
+  auto lap = [&](int i) {
+    const long long t = clock64();
+    clk[i] += (unsigned long long)(t - tc);
+    tc = t;
+  };
   for (;;) {
     // --- level scan: compact the live list, minimum live support
     {
@@ -489,6 +497,7 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       if (ln == 0 && mn != ~0ull) atomicMin(&c->minsup, mn);
     }
     wing_grid_sync(&c->bar, epoch);
+    lap(0);
     cur ^= 1;
     nlive = *(volatile uint32_t*)&c->nlive;
     if (nlive == 0) break;
@@ -506,6 +515,7 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       warp_append(take, e, SX[0], &c->cnt[0]);
     }
     wing_grid_sync(&c->bar, epoch);
+    lap(1);
     if (lead) {  // every thread read them before the barrier above
       c->nlive = 0;
       c->minsup = ~0ull;
@@ -555,6 +565,7 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
         for (uint64_t j = w.inc_off[e] + threadIdx.x; j < w.inc_off[e + 1]; j += blockDim.x) claim(j);
       }
       wing_grid_sync(&c->bar, epoch);
+      lap(2);
       // --- batch bloom update (k_wing_update); crossers go to SX[cs ^ 1]
       const uint32_t nT = *(volatile uint32_t*)&c->nT[r];
       if (lead) c->cnt[cs] = 0;
@@ -613,6 +624,7 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
         }
       }
       wing_grid_sync(&c->bar, epoch);
+      lap(3);
       cs ^= 1;
     }
     if (!any) wing_grid_sync(&c->bar, epoch);  // (cannot happen: the minimum is selected) keeps the reset ordered
@@ -620,6 +632,7 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
   if (lead) {
     c->levels = levels;
     c->rounds = rounds;
+    for (int i = 0; i < 4; i++) c->clk[i] = clk[i];
   }
 }
 

@@ -1562,6 +1562,9 @@ void wing_peel(Run& r, const Dev& gr, const BeIndex& I, uint64_t* theta, uint64_
       info[2] = out.levels;
       info[3] = out.rounds;
     }
+    if (std::getenv("PBNG_TRACE"))
+      std::fprintf(stderr, "wing peel cycles (CTA 0): scan=%llu select=%llu claim=%llu update=%llu\n", out.clk[0],
+                   out.clk[1], out.clk[2], out.clk[3]);
     return;
   }
   w.ctl = r.alloc<WingCtl>(1);
@@ -1636,10 +1639,19 @@ void wing_decompose(const Dev& g, uint64_t* out, uint64_t* info, cudaStream_t s)
   Run r(s);
   SideRank RU, RV;
   const Dev gr = relabel(r, g, RU, RV);
+  const bool trace = std::getenv("PBNG_TRACE") != nullptr;  // phase times on stderr (development aid)
+  cudaEvent_t t0 = trace ? r.event() : nullptr;
   BeIndex I;
   be_build(r, gr, RU, RV, I);
+  cudaEvent_t t1 = trace ? r.event() : nullptr;
   uint64_t* theta = r.alloc<uint64_t>(g.m);
   wing_peel(r, gr, I, theta, info);
+  if (trace) {
+    cudaEvent_t t2 = r.event();
+    CK(cudaStreamSynchronize(r.st));
+    std::fprintf(stderr, "wing: be_index_ms=%.3f peel_ms=%.3f blooms=%llu pairs=%llu\n", elapsed(t0, t1), elapsed(t1, t2),
+                 (unsigned long long)I.nb, (unsigned long long)I.np);
+  }
   r.pre(PBNG_K_INIT);
   k_wing_gather<<<r.nsm * 8, 256, 0, r.st>>>(g.nU, g.m, g.offU, g.adjU, RU.rank, RV.rank, gr.offU, gr.adjU, theta,
                                               out);
