@@ -441,7 +441,8 @@ struct WingDev {
   unsigned long long clk[4];   // CTA 0 thread 0: cycles in level scans, selects, claim phases, update phases
 };
 constexpr uint32_t kWingThreads = 1024;
-constexpr uint32_t kWingBigLen = 512;   // pair lists longer than this are walked by a whole CTA
+constexpr uint32_t kWingBigLen = 32;    // pair lists longer than this are walked by a whole CTA
+constexpr uint32_t kWingBigMax = 1u << 22;  // ... up to this length (the flattened range of a CTA stays below 2^32)
 constexpr uint32_t kWingBigCap = 256;   // ... up to this many per CTA and phase (more: the warp walks them)
 
 __device__ __forceinline__ void wing_grid_sync(unsigned long long* bar, unsigned long long& epoch) {
@@ -461,14 +462,16 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
                                                                   uint32_t* sx0, uint32_t* sx1, WingDev* c) {
   const uint32_t ln = lane_id();
   const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t gw = gt >> 5, nw = nt >> 5;
   const bool lead = gt == 0;
   unsigned long long epoch = 0, k = 0, levels = 0, rounds = 0;
   uint32_t* live[2] = {live0, live1};
   uint32_t* SX[2] = {sx0, sx1};
   uint32_t nlive = (uint32_t)w.m, cur = 0;
-  __shared__ uint32_t big[kWingBigCap];  // per CTA: long pair lists left to the whole CTA
+  __shared__ uint32_t big[kWingBigCap];  // per CTA: long pair lists left to the whole CTA (edge / bloom,
+  __shared__ uint32_t biglen[kWingBigCap], bigpre[kWingBigCap], bigkb[kWingBigCap], bigd[kWingBigCap];  // length, prefix, k_B, d)
+  __shared__ uint32_t scanbuf[33];
   __shared__ uint32_t nbig;
+  const uint32_t wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
   unsigned long long clk[4] = {0, 0, 0, 0};
   long long tc = clock64();
   auto lap = [&](int i) {
@@ -537,32 +540,48 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
         const uint32_t b = w.pair_bloom[p];
         if (atomicAdd(&w.bloom_d[b], 1u) == 0) w.T[atomicAdd(&c->nT[r], 1u)] = b;
       };
+      // S edges go round-robin over the CTAs (edge i to CTA i mod grid), a warp per edge;
+      // pair lists longer than a warp step are left to the whole CTA, which walks all of
+      // its deferred lists as one flattened range (a warp walking 10^3..10^5 pairs alone,
+      // three dependent loads per step, set the length of the round)
       if (threadIdx.x == 0) nbig = 0;
       __syncthreads();
-      for (uint64_t i = gw; i < nS; i += nw) {
+      for (uint64_t i = blockIdx.x + (uint64_t)gridDim.x * wib; i < nS; i += (uint64_t)gridDim.x * nwb) {
         const uint32_t e = __ldcg(S + i);
         if (ln == 0) {
           w.theta[e] = k;
           w.alive[e] = 0;
         }
         const uint64_t j0 = w.inc_off[e], j1 = w.inc_off[e + 1];
-        // an edge in many pairs is left to the whole CTA (below): a warp walking
-        // 10^4..10^5 pairs alone would set the length of the round
         uint32_t slot = kWingBigCap;
-        if (j1 - j0 > kWingBigLen) {
+        if (j1 - j0 > kWingBigLen && j1 - j0 <= kWingBigMax) {
           if (ln == 0) slot = atomicAdd(&nbig, 1u);
           slot = __shfl_sync(kFull, slot, 0);
           if (slot < kWingBigCap) {
-            if (ln == 0) big[slot] = e;
+            if (ln == 0) {
+              big[slot] = e;
+              biglen[slot] = (uint32_t)(j1 - j0);
+            }
             continue;
           }
         }
         for (uint64_t j = j0 + ln; j < j1; j += 32) claim(j);
       }
       __syncthreads();
-      for (uint32_t i = 0, n = min(nbig, kWingBigCap); i < n; i++) {
-        const uint32_t e = big[i];
-        for (uint64_t j = w.inc_off[e] + threadIdx.x; j < w.inc_off[e + 1]; j += blockDim.x) claim(j);
+      {
+        const uint32_t n = min(nbig, kWingBigCap);
+        uint32_t tot;
+        const uint32_t pre = block_excl_scan(threadIdx.x < n ? biglen[threadIdx.x] : 0u, scanbuf, &tot);
+        if (threadIdx.x < n) bigpre[threadIdx.x] = pre;
+        __syncthreads();
+        for (uint32_t f = threadIdx.x; f < tot; f += blockDim.x) {
+          uint32_t lo = 0, hi = n;  // largest j with bigpre[j] <= f
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (bigpre[mid] <= f) lo = mid; else hi = mid;
+          }
+          claim(w.inc_off[big[lo]] + (f - bigpre[lo]));
+        }
       }
       wing_grid_sync(&c->bar, epoch);
       lap(2);
@@ -592,19 +611,24 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       };
       if (threadIdx.x == 0) nbig = 0;
       __syncthreads();
-      for (uint64_t i = gw; i < nT; i += nw) {
+      for (uint64_t i = blockIdx.x + (uint64_t)gridDim.x * wib; i < nT; i += (uint64_t)gridDim.x * nwb) {
         const uint32_t b = __ldcg(w.T + i);
         const uint64_t p0 = w.bloom_off[b], p1 = w.bloom_off[b + 1];
+        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
         uint32_t slot = kWingBigCap;
-        if (p1 - p0 > kWingBigLen) {  // a large bloom is updated by the whole CTA (below)
+        if (p1 - p0 > kWingBigLen && p1 - p0 <= kWingBigMax) {  // a bloom of more than a warp step: the whole CTA, flattened (below)
           if (ln == 0) slot = atomicAdd(&nbig, 1u);
           slot = __shfl_sync(kFull, slot, 0);
           if (slot < kWingBigCap) {
-            if (ln == 0) big[slot] = b;
+            if (ln == 0) {
+              big[slot] = b;
+              biglen[slot] = (uint32_t)(p1 - p0);
+              bigkb[slot] = kb;
+              bigd[slot] = d;
+            }
             continue;
           }
         }
-        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
         for (uint64_t p = p0 + ln; p < p1; p += 32) upd_pair(p, kb, d);
         __syncwarp();
         if (ln == 0) {
@@ -613,14 +637,23 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
         }
       }
       __syncthreads();
-      for (uint32_t i = 0, n = min(nbig, kWingBigCap); i < n; i++) {
-        const uint32_t b = big[i];
-        const uint32_t kb = __ldcg(w.bloom_k + b), d = __ldcg(w.bloom_d + b);
-        for (uint64_t p = w.bloom_off[b] + threadIdx.x; p < w.bloom_off[b + 1]; p += blockDim.x) upd_pair(p, kb, d);
-        __syncthreads();  // every thread has read kb and d
-        if (threadIdx.x == 0) {
-          w.bloom_k[b] = kb - d;
-          w.bloom_d[b] = 0;
+      {
+        const uint32_t n = min(nbig, kWingBigCap);
+        uint32_t tot;
+        const uint32_t pre = block_excl_scan(threadIdx.x < n ? biglen[threadIdx.x] : 0u, scanbuf, &tot);
+        if (threadIdx.x < n) bigpre[threadIdx.x] = pre;
+        __syncthreads();
+        for (uint32_t f = threadIdx.x; f < tot; f += blockDim.x) {
+          uint32_t lo = 0, hi = n;
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (bigpre[mid] <= f) lo = mid; else hi = mid;
+          }
+          upd_pair(w.bloom_off[big[lo]] + (f - bigpre[lo]), bigkb[lo], bigd[lo]);
+        }
+        if (threadIdx.x < n) {  // kb and d of the deferred blooms were taken before any pair was updated
+          w.bloom_k[big[threadIdx.x]] = bigkb[threadIdx.x] - bigd[threadIdx.x];
+          w.bloom_d[big[threadIdx.x]] = 0;
         }
       }
       wing_grid_sync(&c->bar, epoch);
