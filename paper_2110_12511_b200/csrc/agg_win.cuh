@@ -70,6 +70,7 @@ constexpr int kDenseDepth = PBNG_DENSE_DEPTH;
 #define PBNG_DENSE_TOUCH 0
 #endif
 constexpr uint32_t kWinChunk = PBNG_WIN_CHUNK ? PBNG_WIN_CHUNK : 512;  // entries per warp task
+static_assert(kWinChunk % 4 == 0 && PBNG_DENSE_CHUNK % 4 == 0, "chunks are cut at 16-byte aligned positions");
 
 // bitmap windows with many entries use 256-entry chunks read two 16-byte loads
 // per lane at a time (more bytes in flight); smaller ones 128-entry chunks
@@ -281,7 +282,10 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
       S.segS[tid] = s;
       S.segT[tid] = t;
       S.segB[tid] = base;
-      nch = (t - s + chunk - 1) / chunk;
+      // chunks are cut at 16-byte aligned positions of the partner array (chunk is a
+      // multiple of 4): only the first and last chunk of a segment have an unaligned
+      // head / tail, each of which costs seg_visit a load round trip of its own
+      nch = t > s ? (uint32_t)((((base + s) & 3) + (t - s) + chunk - 1) / chunk) : 0u;
     }
     uint32_t tot;
     const uint32_t cp = block_excl_scan(nch, S.scan, &tot);
@@ -304,9 +308,9 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
         if (S.cpre[mid] <= c) lo = mid; else hi = mid;
       }
       const uint64_t base = S.segB[lo];
-      const uint64_t i0 = base + S.segS[lo] + (uint64_t)(c - S.cpre[lo]) * chunk;
-      const uint64_t i1e = base + S.segT[lo];
-      fn(i0, i0 + chunk < i1e ? i0 + chunk : i1e, e0 + bs + lo);
+      const uint64_t i0s = base + S.segS[lo], i1e = base + S.segT[lo];
+      const uint64_t cut = (i0s & ~3ull) + (uint64_t)(c - S.cpre[lo]) * chunk;  // aligned chunk start
+      fn(cut > i0s ? cut : i0s, cut + chunk < i1e ? cut + chunk : i1e, e0 + bs + lo);
     }
     __syncthreads();
     if (pc && tid == 0) {
