@@ -253,7 +253,10 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
                                          uint64_t wb, uint64_t a, uint64_t b, const uint32_t* __restrict__ partner,
                                          WinSmem& S, WinShared& sh, Fn& fn, uint32_t chunk = kWinChunk,
                                          const uint32_t* __restrict__ sub = nullptr, uint32_t sj = 0,
-                                         uint32_t sstride = 0, unsigned long long* pc = nullptr) {
+                                         uint32_t sstride = 0, unsigned long long* pc = nullptr,
+                                         const unsigned long long* __restrict__ gb = nullptr) {
+  // gb (optional, with sub): the list bases the start's tables already hold (one load
+  // instead of the three dependent ones of lists.get, in a phase where one warp works)
   // sub (optional): precomputed bounds of list i's sub-window sj at sub[i * sstride + sj]
   const uint32_t tid = threadIdx.x, ln = lane_id();
   bool any = false;
@@ -264,8 +267,9 @@ __device__ __forceinline__ bool win_pass(const L& lists, uint64_t e0, uint64_t n
     if (tid < nb) {
       const uint64_t i = bs + tid;
       uint64_t base;
-      uint32_t len;
-      lists.get(e0 + i, base, len);
+      uint32_t len = 0;
+      if (gb && sub) base = gb[i];
+      else lists.get(e0 + i, base, len);
       const uint32_t* p = partner + base;
       uint32_t s, t;
       if (sub) {
@@ -672,7 +676,7 @@ __device__ __forceinline__ void win_agg_one(const L& lists, uint64_t e0, uint64_
       const uint32_t chunk = PBNG_DENSE_CHUNK ? PBNG_DENSE_CHUNK : (pre ? win_chunk(S.ek[kr] * SW / kWinIds) : kWinChunk);
       const long long tq0 = prof ? clock64() : 0;
       const bool any = win_pass(lists, e0, nl, pre, bnd, W, k, wa, wb, a, b, partner, S, sh, mark, chunk, sub, sj, 33,
-                                prof ? cnt->prof3 : nullptr);
+                                prof ? cnt->prof3 : nullptr, sub ? gbase : nullptr);
       const long long tq1 = prof ? clock64() : 0;
       if (prof && tid == 0) atomicAdd(&cnt->prof3[1], (unsigned long long)(tq1 - tq0));
       if (!any) continue;
