@@ -439,6 +439,8 @@ struct WingDev {
   unsigned long long bar;      // grid barrier: arrivals so far (monotonic)
   unsigned long long levels, rounds;
   unsigned long long clk[4];   // CTA 0 thread 0: cycles in level scans, selects, claim phases, update phases
+  uint32_t cntC[2];            // candidate band: lengths of the two candidate lists
+  unsigned long long minC;     // minimum live support among the candidates
 };
 constexpr uint32_t kWingThreads = 1024;
 constexpr uint32_t kWingBigLen = 32;    // pair lists longer than this are walked by a whole CTA
@@ -459,13 +461,15 @@ __device__ __forceinline__ void wing_grid_sync(unsigned long long* bar, unsigned
 }
 
 __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint32_t* live0, uint32_t* live1,
-                                                                  uint32_t* sx0, uint32_t* sx1, WingDev* c) {
+                                                                  uint32_t* sx0, uint32_t* sx1, uint32_t* cand0,
+                                                                  uint32_t* cand1, WingDev* c) {
   const uint32_t ln = lane_id();
   const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   const bool lead = gt == 0;
   unsigned long long epoch = 0, k = 0, levels = 0, rounds = 0;
   uint32_t* live[2] = {live0, live1};
   uint32_t* SX[2] = {sx0, sx1};
+  uint32_t* Cand[2] = {cand0, cand1};
   uint32_t nlive = (uint32_t)w.m, cur = 0;
   __shared__ uint32_t big[kWingBigCap];  // per CTA: long pair lists left to the whole CTA (edge / bloom,
   __shared__ uint32_t biglen[kWingBigCap], bigpre[kWingBigCap], bigkb[kWingBigCap], bigd[kWingBigCap];  // length, prefix, k_B, d)
@@ -505,17 +509,24 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
     nlive = *(volatile uint32_t*)&c->nlive;
     if (nlive == 0) break;
     k = max(k, *(volatile unsigned long long*)&c->minsup);
-    levels++;
-    // --- S = live edges with support <= k
+    // --- candidate band: the levels k .. B are peeled from the candidate list C = live edges
+    // with support <= B (an edge whose support falls to <= B later is appended by the update
+    // that takes it there), so the next level is the minimum over C, not over the live list:
+    // the full scan above runs once per band instead of once per level
+    const unsigned long long B = k + max(16ull, k >> 2);
+    // S = live edges with support <= k, C = ... <= B (every listed edge is alive)
     for (uint64_t i0 = gt - ln; i0 < nlive; i0 += nt) {
       const uint64_t i = i0 + ln;
-      bool take = false;
+      bool take = false, cand = false;
       uint32_t e = 0;
       if (i < nlive) {
         e = __ldcg(live[cur] + i);
-        take = __ldcg(w.sup + e) <= k;  // every listed edge is alive (the scan dropped the peeled ones)
+        const unsigned long long s = __ldcg(w.sup + e);
+        take = s <= k;
+        cand = s <= B;
       }
       warp_append(take, e, SX[0], &c->cnt[0]);
+      warp_append(cand, e, Cand[0], &c->cntC[0]);
     }
     wing_grid_sync(&c->bar, epoch);
     lap(1);
@@ -523,6 +534,9 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       c->nlive = 0;
       c->minsup = ~0ull;
     }
+    uint32_t cc = 0;
+    for (;;) {  // levels of the band
+    levels++;
     uint32_t cs = 0;
     bool any = false;
     for (;;) {
@@ -590,9 +604,12 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       if (lead) c->cnt[cs] = 0;
       uint32_t* X = SX[cs ^ 1];
       uint32_t* nX = &c->cnt[cs ^ 1];
+      uint32_t* CL = Cand[cc];
+      uint32_t* nCL = &c->cntC[cc];
       auto dec = [&](uint32_t x, unsigned long long d) {
         const unsigned long long old = atomicAdd(&w.sup[x], (unsigned long long)(0ull - d));
         if (old > k && old - d <= k) X[atomicAdd(nX, 1u)] = x;
+        if (old > B && old - d <= B) CL[atomicAdd(nCL, 1u)] = x;  // enters the band
       };
       auto upd_pair = [&](uint64_t p, uint32_t kb, uint32_t d) {
         const uint32_t st = __ldcg(w.pstate + p);
@@ -661,6 +678,61 @@ __global__ void __launch_bounds__(kWingThreads, 1) k_wing_peel(WingArgs w, uint3
       cs ^= 1;
     }
     if (!any) wing_grid_sync(&c->bar, epoch);  // (cannot happen: the minimum is selected) keeps the reset ordered
+    // --- next level: compact the candidates (drop the peeled), minimum live support among them
+    {
+      const uint32_t nC = *(volatile uint32_t*)&c->cntC[cc];
+      unsigned long long mn = ~0ull;
+      for (uint64_t i0 = gt - ln; i0 < nC; i0 += nt) {
+        const uint64_t i = i0 + ln;
+        bool keep = false;
+        uint32_t e = 0;
+        if (i < nC) {
+          e = __ldcg(Cand[cc] + i);
+          keep = __ldcg(w.alive + e);
+          if (keep) mn = min(mn, __ldcg(w.sup + e));
+        }
+        warp_append(keep, e, Cand[cc ^ 1], &c->cntC[cc ^ 1]);
+      }
+      mn = warp_min_u64(mn);
+      if (ln == 0 && mn != ~0ull) atomicMin(&c->minC, mn);
+    }
+    wing_grid_sync(&c->bar, epoch);
+    lap(0);
+    const uint32_t nC2 = *(volatile uint32_t*)&c->cntC[cc ^ 1];
+    const unsigned long long mnC = *(volatile unsigned long long*)&c->minC;
+    if (nC2 == 0 || mnC > B) {
+      // band exhausted: back to a full scan.  The barrier orders every thread's reads of the
+      // counters before their reset; the scan phase does not touch them.
+      wing_grid_sync(&c->bar, epoch);
+      if (lead) {
+        c->cntC[0] = 0;
+        c->cntC[1] = 0;
+        c->minC = ~0ull;
+      }
+      break;
+    }
+    k = mnC;  // > the level just finished: everything <= it was peeled
+    cc ^= 1;
+    {
+      const uint32_t* CLs = Cand[cc];
+      for (uint64_t i0 = gt - ln; i0 < nC2; i0 += nt) {
+        const uint64_t i = i0 + ln;
+        bool take = false;
+        uint32_t e = 0;
+        if (i < nC2) {
+          e = __ldcg(CLs + i);
+          take = __ldcg(w.sup + e) <= k;
+        }
+        warp_append(take, e, SX[0], &c->cnt[0]);
+      }
+    }
+    wing_grid_sync(&c->bar, epoch);
+    lap(1);
+    if (lead) {  // every thread read them before the barrier above; the rounds do not touch them
+      c->cntC[cc ^ 1] = 0;
+      c->minC = ~0ull;
+    }
+    }  // levels of the band
   }
   if (lead) {
     c->levels = levels;

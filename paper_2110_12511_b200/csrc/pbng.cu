@@ -1548,8 +1548,10 @@ void wing_peel(Run& r, const Dev& gr, const BeIndex& I, uint64_t* theta, uint64_
     WingDev init;
     std::memset(&init, 0, sizeof(init));
     init.minsup = ~0ull;
+    init.minC = ~0ull;
     CK(cudaMemcpyAsync(dc, &init, sizeof(init), cudaMemcpyHostToDevice, r.st));
-    void* args[] = {&w, &live[0], &live[1], &SX[0], &SX[1], &dc};
+    uint32_t* cand[2] = {r.alloc<uint32_t>(m), r.alloc<uint32_t>(m)};  // candidate band lists
+    void* args[] = {&w, &live[0], &live[1], &SX[0], &SX[1], &cand[0], &cand[1], &dc};
     r.pre(PBNG_K_FD);
     CK(cudaLaunchCooperativeKernel((const void*)k_wing_peel, dim3(r.nsm), dim3(kWingThreads), args, 0, r.st));
     r.post(PBNG_K_FD);
